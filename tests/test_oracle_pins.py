@@ -1,0 +1,223 @@
+"""Pins of the CPU oracle against things other than itself (CPU only).
+
+Each pin is chosen so that a plausible mistake in the oracle (a dropped
+diagonal or transposed term, a wrong index, a transposed operand, a missing
+island rule, a wrong level) fails at least one of them.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.csgraph as csg
+
+import gen
+import oracle
+
+U_EPS = 2.0 ** -53
+
+
+def relinf(a, b):
+    d = np.max(np.abs(np.asarray(a, dtype=np.float64) - np.asarray(b, dtype=np.float64))) if len(a) else 0.0
+    s = np.max(np.abs(b)) if len(b) else 0.0
+    return d / s if s > 0 else d
+
+
+def scipy_full(U):
+    """A = U + U^T - diag(U) with scipy (a library routine, independent of the oracle)."""
+    Us = sp.csr_matrix((U.val, U.col, U.row_ptr), shape=(U.n, U.n))
+    return (Us + Us.T - sp.diags(Us.diagonal())).tocsr()
+
+
+SMALL = [
+    lambda: gen.lap2d(7),
+    lambda: gen.st27(5, 2, True),
+    lambda: gen.spin(7, 4),
+    lambda: gen.knn(150, 6, 3),
+    lambda: gen.lap3d(5, 5, True),
+    lambda: gen.random_symmetric(180, 6.0, 1),
+    lambda: gen.random_symmetric(97, 2.5, 2, diag_frac=0.6),
+    lambda: gen.banded_random(120, 9, 5.0, 3),
+]
+
+
+# --------------------------------------------------------------- SymmSpMV pins
+@pytest.mark.parametrize("mk", SMALL)
+def test_symmspmv_vs_dense_bruteforce(mk):
+    """y = A x by the definition y_i = sum_j A_ij x_j on the dense matrix."""
+    U = mk()
+    x = gen.vector_uniform(U.n, 7)
+    Ad = oracle.to_dense(U)
+    y_dense = Ad @ x  # numpy, independent summation
+    y = oracle.symmspmv(U, x)
+    assert relinf(y, y_dense) <= 1e-14
+    assert relinf(oracle.dense_matvec(Ad, x), y_dense) <= 1e-14
+
+
+@pytest.mark.parametrize("mk", SMALL)
+def test_symmspmv_vs_scipy_and_spmv_identity(mk):
+    """SymmSpMV(U) == SpMV(A), A mirrored two independent ways."""
+    U = mk()
+    x = gen.vector_uniform(U.n, 11)
+    A = scipy_full(U)
+    y_sc = A @ x
+    frp, fcol, fval = oracle.mirror(U)
+    assert np.array_equal(frp, A.indptr.astype(np.int32))
+    As = A.copy()
+    As.sort_indices()
+    assert np.array_equal(fcol, As.indices) and np.array_equal(fval, As.data)
+    y_spmv = oracle.spmv(frp, fcol, fval, x)
+    y = oracle.symmspmv(U, x)
+    assert relinf(y, y_sc) <= 1e-13
+    assert relinf(y_spmv, y_sc) <= 1e-13
+    assert relinf(y, y_spmv) <= 1e-13
+
+
+def test_laplacian_eigenpair_closed_form():
+    """2-D 5-pt Laplacian, x_ij = sin(pi i/(N+1)) sin(pi j/(N+1)) -> A x = lambda x,
+    lambda = 4 - 4 cos(pi/(N+1)) (north_star).  Backward-error bound (reading R6)."""
+    N = 64
+    U = gen.lap2d(N)
+    x = gen.vector_sinsin(N)
+    lam = 4.0 - 4.0 * math.cos(math.pi / (N + 1))
+    assert abs(lam - 0.004671092670693433) < 1e-17
+    y = oracle.symmspmv(U, x)
+    err = np.max(np.abs(y - lam * x))
+    assert err <= 8 * U_EPS * 8.0 * np.max(np.abs(x))
+    # a dropped transposed term would leave O(1) errors:
+    assert err < 1e-13
+
+
+def test_spec_hand_cases():
+    # [[2,1],[1,3]] . [1,1] = [3,4]
+    U = gen.from_edges(2, [0], [1], [1.0], [2.0, 3.0])
+    assert np.array_equal(oracle.symmspmv(U, np.array([1.0, 1.0])), [3.0, 4.0])
+    # diagonal only -> b_i = d_i x_i
+    d = np.array([1.5, -2.0, 3.25, 0.0])
+    U = gen.from_edges(4, [], [], [], d)
+    x = np.array([2.0, 3.0, -1.0, 9.0])
+    assert np.array_equal(oracle.symmspmv(U, x), d * x)
+    # single bond (0,1) = v with zero diagonal -> [v x1, v x0]
+    U = gen.from_edges(2, [1], [0], [0.5], [0.0, 0.0])
+    assert np.array_equal(oracle.symmspmv(U, np.array([3.0, 5.0])), [2.5, 1.5])
+    # rows without a stored diagonal contribute no diagonal term (reading R1)
+    U = gen.from_edges(3, [0, 1], [1, 2], [1.0, 2.0], [7.0, 7.0, 7.0], has_diag=[0, 1, 0])
+    assert np.array_equal(oracle.symmspmv(U, np.array([1.0, 1.0, 1.0])), [1.0, 10.0, 2.0])
+
+
+def test_empty_and_single():
+    U = gen.from_edges(0, [], [], [], np.zeros(0))
+    assert oracle.symmspmv(U, np.zeros(0)).shape == (0,)
+    U = gen.from_edges(1, [], [], [], [2.5])
+    assert oracle.symmspmv(U, np.array([4.0]))[0] == 10.0
+
+
+def test_linearity_and_long_double():
+    U = gen.random_symmetric(300, 8.0, 5)
+    x, z = gen.vector_uniform(U.n, 1), gen.vector_uniform(U.n, 2)
+    a, b = 0.75, -1.25
+    lhs = oracle.symmspmv(U, a * x + b * z)
+    rhs = a * oracle.symmspmv(U, x) + b * oracle.symmspmv(U, z)
+    assert relinf(lhs, rhs) <= 1e-13
+    yl = oracle.symmspmv_ld(U, x)
+    assert relinf(oracle.symmspmv(U, x), yl.astype(np.float64)) <= 1e-14
+
+
+def test_write_conflicts_two_ways():
+    for U in (gen.random_symmetric(60, 4.0, 9), gen.lap2d(6)):
+        pairs = oracle.conflicting_row_pairs(U)
+        cls = np.zeros(U.n, dtype=np.int32)
+        assert oracle.write_conflicts(U, cls) == len(pairs)
+        # each row its own class -> no conflicts
+        assert oracle.write_conflicts(U, np.arange(U.n, dtype=np.int32)) == 0
+    # hand case: rows 0 and 1 both write b[2]
+    U = gen.from_edges(3, [0, 1], [2, 2])
+    assert oracle.conflicting_row_pairs(U) == {(0, 2), (1, 2), (0, 1)}
+
+
+# --------------------------------------------------------------- BFS level pins
+def _levels(dist):
+    tl = int(dist.max()) + 1 if len(dist) else 0
+    return np.bincount(dist, minlength=tl)
+
+
+def test_bfs_path_star_islands():
+    # path 0-1-2-3-4, root 0 -> level_ptr = [0,1,2,3,4,5]
+    gp, ga = oracle.graph(gen.path(5))
+    dist, tl = oracle.bfs_levels(gp, ga, [0])
+    assert tl == 5 and list(dist) == [0, 1, 2, 3, 4]
+    # two islands {0-1}, {2-3}, root 0 -> L(2) empty
+    gp, ga = oracle.graph(gen.from_edges(4, [0, 2], [1, 3]))
+    dist, tl = oracle.bfs_levels(gp, ga, [0])
+    assert list(dist) == [0, 1, 3, 4] and tl == 5
+    # star with centre as root -> totalLvl = 2
+    gp, ga = oracle.graph(gen.from_edges(6, [3] * 5, [0, 1, 2, 4, 5]))
+    dist, tl = oracle.bfs_levels(gp, ga, [3])
+    assert tl == 2 and dist[3] == 0 and sorted(dist) == [0, 1, 1, 1, 1, 1]
+
+
+def test_bfs_grid_closed_forms():
+    N = 9
+    gp, ga = oracle.graph(gen.lap2d(N))
+    dist, tl = oracle.bfs_levels(gp, ga, [0])
+    assert tl == 2 * N - 1
+    assert list(_levels(dist)) == [min(s + 1, 2 * N - 1 - s) for s in range(2 * N - 1)]
+    # 7-pt N^3 from a corner: level s = #{(i,j,k) in [0,N)^3 : i+j+k = s}
+    N = 7
+    gp, ga = oracle.graph(gen.lap3d(N, 5, False))
+    dist, tl = oracle.bfs_levels(gp, ga, [0])
+    i, j, k = np.meshgrid(np.arange(N), np.arange(N), np.arange(N), indexing="ij")
+    assert tl == 3 * N - 2
+    assert np.array_equal(_levels(dist), np.bincount((i + j + k).ravel()))
+    # 27-pt N^3 (unshuffled) from a corner: Chebyshev shells (d+1)^3 - d^3
+    gp, ga = oracle.graph(gen.st27(N, 2, False))
+    dist, tl = oracle.bfs_levels(gp, ga, [0])
+    assert tl == N and list(_levels(dist)) == [(d + 1) ** 3 - d ** 3 for d in range(N)]
+
+
+def test_bfs_spin_components_binomial():
+    """i XOR (3<<b) keeps popcount parity: 2 components; levels C(L-1, d)."""
+    L = 10
+    U = gen.spin(L, 4)
+    gp, ga = oracle.graph(U)
+    ncomp, lab = csg.connected_components(scipy_full(U), directed=False)
+    assert ncomp == 2
+    dist, tl = oracle.bfs_levels(gp, ga, [0])
+    comp0 = dist[lab == lab[0]]
+    assert list(np.bincount(comp0)) == [math.comb(L - 1, d) for d in range(L)]
+    # second island starts at level (L-1) + 2
+    comp1 = dist[lab != lab[0]]
+    assert comp1.min() == (L - 1) + 2
+    assert tl == 2 * L + 1
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_bfs_vs_scipy_shortest_path_and_corollary(seed):
+    U = gen.random_symmetric(200, 3.0, seed)
+    gp, ga = oracle.graph(U)
+    A = abs(scipy_full(U))
+    root = 5
+    D = csg.shortest_path(A, unweighted=True, directed=False)
+    ncomp, lab = csg.connected_components(A, directed=False)
+    dist, tl = oracle.bfs_levels(gp, ga, [root])
+    comp = lab == lab[root]
+    assert np.array_equal(dist[comp], D[root, comp].astype(np.int32))
+    # |level(u) - level(v)| <= 1 on every edge inside a component
+    rows = np.repeat(np.arange(U.n), np.diff(gp))
+    assert np.all(np.abs(dist[rows] - dist[ga]) <= 1)
+    # corollary_dk: level gap >= k+1 => distance > k
+    for k in (1, 2, 3):
+        gap = np.abs(dist[:, None] - dist[None, :]) >= k + 1
+        assert np.all(D[gap] > k)
+
+
+def test_distk_bruteforce_path():
+    gp, ga = oracle.graph(gen.path(30))
+    D = csg.shortest_path(abs(scipy_full(gen.path(30))), unweighted=True, directed=False)
+    for k in (1, 2, 3):
+        good = (np.arange(30) % (k + 1)).astype(np.int32)
+        assert oracle.distk_violations(gp, ga, k, good) == 0
+        bad = (np.arange(30) % k).astype(np.int32) if k > 1 else np.zeros(30, np.int32)
+        expect = int(np.sum((D <= k) & (D > 0) & (bad[:, None] == bad[None, :])))
+        got = oracle.distk_violations(gp, ga, k, bad)
+        assert got == expect and got > 0
