@@ -1,0 +1,187 @@
+/* symmspmv.h — C ABI of the B200 SymmSpMV library (libsymmspmv.so).
+ *
+ * Operation (the hot path this library exists for): SymmSpMV
+ * (§3.2, Alg. 2 alg:SymmSpMV): given the upper triangle U (diagonal included)
+ * of a symmetric sparse matrix A = U + U^T - diag(U) in CRS with 8-byte values
+ * and 4-byte indices, compute
+ *
+ *        y := A x        (every stored a_ij, i < j, updates y_i += a_ij x_j
+ *                         and y_j += a_ij x_i; the diagonal contributes once)
+ *
+ * Alg. 2 accumulates into b with `+=`; this ABI overwrites
+ * y (reading R2).  Rows without a stored diagonal are accepted and
+ * contribute no diagonal term (reading R1).
+ *
+ * The RACE preprocessing (§4) that makes SymmSpMV parallel
+ * without write conflicts lives in race_build_schedule(): BFS levels (§4.1,
+ * Alg. 3), level permutation, distance-k level groups (§4.2), epsilon level
+ * aggregation (§4.4.3) and Alg. 4 load balancing (§4.3), then the GPU
+ * adaptation: contiguous tiles per level group, exact tile write-conflict
+ * coloring and intra-tile distance-2 row coloring.
+ *
+ * Conventions for every call:
+ *   - 0-based indices, half-open ranges.
+ *   - Return value: SYMM_OK (0) or a negative symm_status.  On error nothing
+ *     is allocated / nothing is launched; symm_last_error() returns a
+ *     thread-local message naming the first offending row/column.
+ *   - "HOST" pointers are read during the call only; the library copies what
+ *     it keeps.  "DEVICE" pointers must be device memory of the plan's device.
+ *   - No call takes or returns a torch type.
+ */
+#ifndef SYMMSPMV_H
+#define SYMMSPMV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SYMM_OK = 0,
+  SYMM_ERR_ARG = -1,        /* NULL / negative size / bad option value            */
+  SYMM_ERR_NOT_UPPER = -2,  /* a stored col < row, or col >= n                    */
+  SYMM_ERR_UNSORTED = -3,   /* columns of a row not strictly ascending (dups)     */
+  SYMM_ERR_OVERFLOW = -4,   /* nnz >= 2^31 or n >= 2^31 (int32 CRS) */
+  SYMM_ERR_OOM = -5,        /* host or device allocation failed                   */
+  SYMM_ERR_CUDA = -6,       /* a CUDA runtime call failed (message has the error) */
+  SYMM_ERR_NCCL = -7,       /* multi-GPU communicator failure                     */
+  SYMM_ERR_MISMATCH = -8,   /* matrix does not match the schedule it is used with */
+  SYMM_ERR_ALIAS = -9,      /* x and y overlap                                    */
+  SYMM_ERR_SCHEDULE = -10,  /* internal schedule validator failed (a bug)         */
+  SYMM_ERR_K = -11,         /* distance k < 2 requested for SymmSpMV*/
+  SYMM_ERR_UNSUPPORTED = -12/* variant cannot run this matrix (e.g. tile > smem)  */
+} symm_status;
+
+/* Upper-triangular CRS (double A[nnz]; int col[nnz],
+ * rowPtr[nrows+1]).  HOST pointers, caller-owned.  row_ptr[0] = 0,
+ * row_ptr[n] = nnz, col[row_ptr[r]..row_ptr[r+1]) strictly ascending, all >= r. */
+typedef struct {
+  int32_t n;
+  int64_t nnz;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+} symm_csr_upper;
+
+/* Schedule-builder options (defaults from race_config_default). */
+typedef struct {
+  int32_t k;                /* distance of the coloring; SymmSpMV needs 2 */
+  int32_t n_workers;        /* workers (GPU tiles) for eps aggregation; 0 = derive from work  */
+  int32_t tile_work;        /* target work per tile when n_workers == 0 (nnz + 2 rows units) */
+  int32_t balance_by;       /* 0 = rows, 1 = nnz + 2 rows                */
+  int32_t root;             /* BFS root of the first island; -1 = pseudo-peripheral           */
+  int32_t n_eps;            /* number of valid eps[] entries                                 */
+  double eps[8];            /* eps_s per stage (0.8, 0.8, 0.5 ...)             */
+  int32_t max_tile_rows;    /* hard cap on rows per tile (<= 65535)                          */
+  int32_t max_tile_window;  /* cap on |own rows ∪ targets| per tile (smem entries)           */
+  int32_t reorder;          /* 1 = BFS level permutation; 0 = keep order */
+  int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
+  uint32_t flags;           /* reserved, 0                                                   */
+} race_config;
+
+typedef struct race_schedule race_schedule_t;
+
+typedef struct {
+  int32_t n, total_levels, n_components, n_groups, n_tiles, n_phases;
+  int32_t max_subcolors, max_tile_window, max_tile_rows, n_dag_edges;
+  int64_t nnz, bandwidth_before, bandwidth_after;
+  double eta;               /* §5 parallel efficiency of the tile tree (work = balance unit) */
+  double build_seconds;
+  double mean_subcolors;
+  int64_t spill_entries;    /* sum over tiles of |targets outside own rows|                 */
+} race_schedule_stats;
+
+void race_config_default(race_config* cfg);
+
+/* Builds the RACE schedule for U (HOST).  *out is owned by the caller until
+ * race_schedule_destroy.  Deterministic: same U + cfg => same schedule. */
+int race_build_schedule(const symm_csr_upper* U, const race_config* cfg, race_schedule_t** out);
+int race_schedule_get_stats(const race_schedule_t* s, race_schedule_stats* out);
+
+/* perm_old2new[old] = new, inv_new2old[new] = old (HOST int32[n] each, caller-allocated). */
+int race_schedule_permutation(const race_schedule_t* s, int32_t* perm_old2new, int32_t* inv_new2old);
+
+/* Generic table access for tests/tools.  `which` names one int32 table; the
+ * call returns its length in *len and copies it to out when out != NULL.
+ *   "level_ptr"   [total_levels+1] row ranges of L(i) in the permuted order
+ *   "dist"        [n] BFS level of every ORIGINAL vertex (Eq. 5)
+ *   "roots"       [n_components] start vertex (original id) of every island
+ *   "group_lvl"   [n_groups+1] level-group pointers T_ptr
+ *   "group_workers" [n_groups] tiles per group (eps aggregation b)
+ *   "tile_ptr"    [n_tiles+1] row ranges of tiles (permuted order)
+ *   "tile_group"  [n_tiles] level group of each tile
+ *   "tile_phase"  [n_tiles] phase = stage-0 color * C + tile color
+ *   "tile_order"  [n_tiles] claim order of the dataflow kernel (topological)
+ *   "dag_ptr"/"dag_pred" predecessor tiles (CSR over tiles)
+ *   "row_subcolor" [n] intra-tile color of every permuted row
+ *   "window_levels" [3*n_windows] (first, end, b) of the eps windows           */
+int race_schedule_table(const race_schedule_t* s, const char* which, int64_t* len, int32_t* out);
+
+/* Permuted upper CRS U' = upper(P A P^T) the plan uses (HOST, caller-allocated:
+ * row_ptr[n+1], col[nnz], val[nnz]); any pointer may be NULL to skip it. */
+int race_schedule_permuted_matrix(const race_schedule_t* s, int32_t* row_ptr, int32_t* col, double* val);
+void race_schedule_destroy(race_schedule_t* s);
+
+/* ---- execution ---------------------------------------------------------- */
+typedef enum {
+  SYMM_VARIANT_AUTO = 0,    /* tiled if every tile fits, else colored                 */
+  SYMM_VARIANT_COLORED = 1, /* K2: one launch per phase, global read-modify-write     */
+  SYMM_VARIANT_ATOMIC = 2,  /* K1: one launch, native fp64 RED for transposed updates */
+  SYMM_VARIANT_TILED = 3    /* K3: persistent dataflow kernel, smem windows, ordered  */
+} symm_variant;
+
+typedef enum { SYMM_ORDER_PERMUTED = 0, SYMM_ORDER_ORIGINAL = 1 } symm_vec_order;
+
+typedef struct {
+  int32_t variant;          /* symm_variant                                             */
+  int32_t device;           /* CUDA device ordinal                                      */
+  int32_t vec_order;        /* symm_vec_order of x/y passed to symmspmv_run              */
+  int32_t nranks, rank;     /* multi-GPU row-block split (1, 0 = single GPU)            */
+  int32_t vec_width;        /* lanes per row (1,2,4,8,16,32); 0 = from SymmNNZR          */
+  int32_t ctas_per_sm;      /* persistent grid of the tiled kernel; 0 = default         */
+  int32_t build_all;        /* 1 = upload tables of every variant (tests)               */
+} symmspmv_options;
+
+typedef struct symmspmv_plan symmspmv_plan_t;
+
+void symmspmv_options_default(symmspmv_options* o);
+
+/* Uploads the schedule's permuted matrix and tables to o->device.  The plan
+ * owns all device memory it allocates; s may be destroyed afterwards.  U must
+ * be the matrix s was built from (checked: n, nnz; else SYMM_ERR_MISMATCH). */
+int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symmspmv_options* o,
+                  symmspmv_plan_t** out);
+
+/* This rank's row slice [row_begin, row_end) of the permuted order. */
+int symmspmv_plan_rows(const symmspmv_plan_t* p, int32_t* row_begin, int32_t* row_end);
+
+/* y := A x on `stream` (a cudaStream_t; NULL = default stream), asynchronous.
+ * x_dev, y_dev: DEVICE fp64[n] in the plan's vec_order; must not overlap
+ * (SYMM_ERR_ALIAS).  `variant` overrides the plan's variant when >= 0 (it
+ * must have been uploaded).  Not re-entrant per plan (one run at a time). */
+int symmspmv_run(symmspmv_plan_t* p, const double* x_dev, double* y_dev, void* stream);
+int symmspmv_run_variant(symmspmv_plan_t* p, int32_t variant, const double* x_dev, double* y_dev,
+                         void* stream);
+
+/* End-to-end convenience: x_host, y_host are HOST fp64[n] in ORIGINAL order
+ * (pinned memory recommended).  H2D copy, permute, run, unpermute, D2H copy,
+ * all on `stream`; returns after the stream has been synchronised. */
+int symmspmv_run_host(symmspmv_plan_t* p, const double* x_host, double* y_host, void* stream);
+
+/* Number of kernel launches the last symmspmv_run issued (evidence for bench). */
+int symmspmv_last_launches(const symmspmv_plan_t* p);
+
+/* Device bytes the plan holds, and the algorithmic bytes of one multiply for
+ * the chosen variant (12 nnz + 4 (n+1) + 24 n). */
+int symmspmv_plan_bytes(const symmspmv_plan_t* p, int64_t* device_bytes, int64_t* min_bytes);
+
+int symmspmv_destroy(symmspmv_plan_t* p);
+
+const char* symm_status_string(int status);
+const char* symm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYMMSPMV_H */

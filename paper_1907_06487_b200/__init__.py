@@ -1,0 +1,184 @@
+"""B200-native SymmSpMV (arXiv 1907.06487, RACE) — thin Python binding.
+
+Argument marshalling only: every step of the hot path runs inside
+``libsymmspmv.so`` (include/symmspmv.h): the RACE schedule builder (C++) and
+the sm_100a kernels.  There is no CPU fallback; importing this package fails
+loudly when the native library is missing.  PyTorch is used only for device
+memory, streams and ``torch.distributed``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _lib
+from ._lib import (SYMM_ORDER_ORIGINAL, SYMM_ORDER_PERMUTED, VARIANTS, SymmError, check, lib)
+
+__all__ = ["build_schedule", "Schedule", "Plan", "VARIANTS", "SymmError", "min_bytes", "flops",
+           "SYMM_ORDER_PERMUTED", "SYMM_ORDER_ORIGINAL", "library_path"]
+
+library_path = _lib.LIB_PATH
+
+
+def _csr_struct(U):
+    rp = np.ascontiguousarray(U.row_ptr, dtype=np.int32)
+    col = np.ascontiguousarray(U.col, dtype=np.int32)
+    val = np.ascontiguousarray(U.val, dtype=np.float64)
+    s = _lib.SymmCsrUpper(int(U.n), int(rp[-1]) if len(rp) else 0, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                          col.ctypes.data_as(C.POINTER(C.c_int32)), val.ctypes.data_as(C.POINTER(C.c_double)))
+    return s, (rp, col, val)
+
+
+def min_bytes(n: int, nnz_u: int) -> int:
+    """Algorithmic bytes of one SymmSpMV: Eq. 3 at alpha = 1/SymmNNZR:
+    12 B per stored upper nonzero, 4 B per row pointer, x read once, y read+written once."""
+    return 12 * nnz_u + 4 * (n + 1) + 24 * n
+
+
+def flops(nnz_full: int) -> int:
+    """2 flops per nonzero of the full symmetric matrix (north_star)."""
+    return 2 * nnz_full
+
+
+class Schedule:
+    """race_schedule_t: BFS levels, permutation, level groups, tiles, colours, DAG."""
+
+    def __init__(self, handle, n):
+        self._h = handle
+        self.n = n
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().race_schedule_destroy(self._h)
+            self._h = None
+
+    @property
+    def stats(self) -> dict:
+        st = _lib.RaceScheduleStats()
+        check(lib().race_schedule_get_stats(self._h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in _lib.RaceScheduleStats._fields_}
+
+    def table(self, name: str) -> np.ndarray:
+        ln = C.c_int64(0)
+        check(lib().race_schedule_table(self._h, name.encode(), C.byref(ln), None))
+        out = np.empty(ln.value, dtype=np.int32)
+        if ln.value:
+            check(lib().race_schedule_table(self._h, name.encode(), C.byref(ln), out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out
+
+    def permutation(self):
+        perm = np.empty(self.n, dtype=np.int32)
+        inv = np.empty(self.n, dtype=np.int32)
+        if self.n:
+            check(lib().race_schedule_permutation(self._h, perm.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  inv.ctypes.data_as(C.POINTER(C.c_int32))))
+        return perm, inv
+
+    def permuted_matrix(self):
+        nnz = self.stats["nnz"]
+        rp = np.empty(self.n + 1, dtype=np.int32)
+        col = np.empty(nnz, dtype=np.int32)
+        val = np.empty(nnz, dtype=np.float64)
+        check(lib().race_schedule_permuted_matrix(self._h, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  col.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  val.ctypes.data_as(C.POINTER(C.c_double))))
+        return rp, col, val
+
+
+def default_config() -> dict:
+    cfg = _lib.RaceConfig()
+    lib().race_config_default(C.byref(cfg))
+    d = {f: getattr(cfg, f) for f, _ in _lib.RaceConfig._fields_}
+    d["eps"] = list(cfg.eps)
+    return d
+
+
+def build_schedule(U, **overrides) -> Schedule:
+    """race_build_schedule(U, cfg): U has n, row_ptr, col, val (numpy, upper CRS)."""
+    cfg = _lib.RaceConfig()
+    lib().race_config_default(C.byref(cfg))
+    for k, v in overrides.items():
+        if k == "eps":
+            for i, e in enumerate(v):
+                cfg.eps[i] = e
+            cfg.n_eps = len(v)
+        elif hasattr(cfg, k):
+            setattr(cfg, k, v)
+        else:
+            raise TypeError(f"unknown race_config field {k}")
+    s, keep = _csr_struct(U)
+    h = C.c_void_p()
+    check(lib().race_build_schedule(C.byref(s), C.byref(cfg), C.byref(h)))
+    return Schedule(h, int(U.n))
+
+
+def _ptr(t):
+    """Device pointer of a torch CUDA float64 tensor (or a raw int)."""
+    if isinstance(t, int):
+        return t
+    import torch
+
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError("expected a contiguous CUDA float64 tensor")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Plan:
+    """symmspmv_plan_t: device-resident matrix + tables for one schedule."""
+
+    def __init__(self, sched: Schedule, U=None, variant="auto", device: int = 0, vec_order="permuted",
+                 vec_width: int = 0, build_all: bool = False):
+        o = _lib.SymmOptions()
+        lib().symmspmv_options_default(C.byref(o))
+        o.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+        o.device = device
+        o.vec_order = SYMM_ORDER_ORIGINAL if vec_order == "original" else SYMM_ORDER_PERMUTED
+        o.vec_width = vec_width
+        o.build_all = int(build_all)
+        h = C.c_void_p()
+        if U is not None:
+            s, keep = _csr_struct(U)
+            check(lib().symmspmv_plan(sched._h, C.byref(s), C.byref(o), C.byref(h)))
+        else:
+            check(lib().symmspmv_plan(sched._h, None, C.byref(o), C.byref(h)))
+        self._h = h
+        self.n = sched.n
+        self.device = device
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().symmspmv_destroy(self._h)
+            self._h = None
+
+    def run(self, x, y, stream=None, variant=None):
+        """y := A x (device tensors, asynchronous on `stream`)."""
+        v = -1 if variant is None else (VARIANTS[variant] if isinstance(variant, str) else int(variant))
+        check(lib().symmspmv_run_variant(self._h, v, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)),
+                                         C.c_void_p(_stream(stream))))
+
+    def run_host(self, x: np.ndarray, y: np.ndarray, stream=None):
+        """End to end: HOST fp64 vectors in ORIGINAL order (pinned recommended)."""
+        check(lib().symmspmv_run_host(self._h, C.c_void_p(x.ctypes.data if isinstance(x, np.ndarray) else x),
+                                      C.c_void_p(y.ctypes.data if isinstance(y, np.ndarray) else y),
+                                      C.c_void_p(_stream(stream))))
+
+    @property
+    def last_launches(self) -> int:
+        return int(lib().symmspmv_last_launches(self._h))
+
+    def bytes(self):
+        d, m = C.c_int64(0), C.c_int64(0)
+        check(lib().symmspmv_plan_bytes(self._h, C.byref(d), C.byref(m)))
+        return d.value, m.value

@@ -1,0 +1,612 @@
+// C ABI of libsymmspmv.so (include/symmspmv.h): schedule objects, plans
+// (device upload of the variant formats), runs.  Host code compiled by nvcc.
+#include <cuda_runtime.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace symm {
+const char* last_error();
+}
+
+struct race_schedule {
+  symm::Schedule S;
+};
+
+using namespace symm;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct symmspmv_plan {
+  int device = 0;
+  int variant = SYMM_VARIANT_AUTO;
+  int vec = 4;
+  int sms = 148;
+  int vec_order = SYMM_ORDER_PERMUTED;
+  int32_t n = 0;
+  int64_t nnz = 0;
+  int nranks = 1, rank = 0;
+  int32_t row_begin = 0, row_end = 0;
+  std::vector<DevBuf> bufs;
+  int64_t device_bytes = 0;
+  // K1 / K2: permuted CRS
+  bool has_csr = false;
+  int32_t *d_rp = nullptr, *d_col = nullptr;
+  double* d_val = nullptr;
+  // K2
+  bool has_colored = false;
+  int32_t *d_tile_ptr = nullptr, *d_phase_tiles = nullptr, *d_srow = nullptr, *d_tile_sub_ptr = nullptr,
+          *d_sub_ptr = nullptr;
+  std::vector<int32_t> phase_off;  // host: offsets of phases in d_phase_tiles
+  // K3
+  bool has_tiled = false;
+  TiledArgs targs{};
+  int tiled_grid = 0;
+  // vector order / host staging
+  int32_t *d_perm = nullptr, *d_inv = nullptr;
+  double *d_xp = nullptr, *d_yp = nullptr;
+  int last_launches = 0;
+  int64_t min_bytes = 0;
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(SYMM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+template <class T>
+int dev_alloc(symmspmv_plan_t* P, T** out, size_t count) {
+  void* p = nullptr;
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(SYMM_ERR_OOM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  P->bufs.push_back({p, bytes});
+  P->device_bytes += (int64_t)bytes;
+  *out = (T*)p;
+  return SYMM_OK;
+}
+
+template <class T>
+int upload(symmspmv_plan_t* P, T** out, const T* host, size_t count) {
+  int rc = dev_alloc(P, out, count);
+  if (rc) return rc;
+  if (count) {
+    cudaError_t e = cudaMemcpy(*out, host, count * sizeof(T), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
+  }
+  return SYMM_OK;
+}
+
+void free_plan(symmspmv_plan_t* P) {
+  if (!P) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(P->device);
+  for (auto& b : P->bufs) cudaFree(b.p);
+  cudaSetDevice(cur);
+  delete P;
+}
+
+int pick_vec(int64_t nnz, int32_t n) {
+  double avg = n > 0 ? (double)nnz / (double)n : 1.0;  // SymmNNZR (Eq. 4 with the diagonal)
+  int v = 1;
+  while (v < 32 && v < avg) v *= 2;
+  return std::max(v, 2);
+}
+
+int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
+  const int32_t nt = (int32_t)S.tile_order.size();
+  const int cap = S.cfg.max_tile_window;
+  if (S.max_window > cap || S.max_window > 65535 || S.max_rows > 65535)
+    return set_error(SYMM_ERR_UNSUPPORTED, "a tile window (%d) exceeds the shared-memory cap (%d)", S.max_window, cap);
+  std::vector<TileDesc> desc((size_t)nt);
+  std::vector<int64_t> nnz_off((size_t)nt + 1, 0);
+  std::vector<int32_t> srow_off((size_t)nt + 1, 0), spill_off((size_t)nt + 1, 0), sub_off((size_t)nt + 1, 0),
+      pred_off((size_t)nt + 1, 0), flag_off((size_t)nt + 1, 0);
+  for (int32_t ti = 0; ti < nt; ++ti) {
+    const int32_t t = S.tile_order[(size_t)ti];
+    const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1];
+    nnz_off[(size_t)ti + 1] = nnz_off[(size_t)ti] + (S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0]);
+    srow_off[(size_t)ti + 1] = srow_off[(size_t)ti] + (r1 - r0);
+    spill_off[(size_t)ti + 1] = spill_off[(size_t)ti] + (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
+    sub_off[(size_t)ti + 1] = sub_off[(size_t)ti] + (S.tile_sub_ptr[(size_t)t + 1] - S.tile_sub_ptr[(size_t)t]);
+    pred_off[(size_t)ti + 1] = pred_off[(size_t)ti] + (S.dag_ptr[(size_t)t + 1] - S.dag_ptr[(size_t)t]);
+    flag_off[(size_t)ti + 1] = flag_off[(size_t)ti] + (r1 - r0 + 31) / 32;
+  }
+  std::vector<uint16_t> lcol((size_t)nnz_off[(size_t)nt]), lrow((size_t)srow_off[(size_t)nt]);
+  std::vector<double> val((size_t)nnz_off[(size_t)nt]);
+  std::vector<int32_t> start((size_t)srow_off[(size_t)nt] + (size_t)nt), spill((size_t)spill_off[(size_t)nt]),
+      sub((size_t)sub_off[(size_t)nt]), pred((size_t)pred_off[(size_t)nt]);
+  std::vector<uint32_t> flags((size_t)flag_off[(size_t)nt], 0);
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 8) reduction(| : bad)
+  for (int32_t ti = 0; ti < nt; ++ti) {
+    const int32_t t = S.tile_order[(size_t)ti];
+    const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
+    const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
+    const int32_t ns = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
+    TileDesc& D = desc[(size_t)ti];
+    std::memset(&D, 0, sizeof D);
+    D.row0 = r0;
+    D.nrows = T;
+    D.nspill = ns;
+    D.nsub = S.tile_sub_ptr[(size_t)t + 1] - S.tile_sub_ptr[(size_t)t] - 1;
+    D.nnz_off = nnz_off[(size_t)ti];
+    D.srow_off = srow_off[(size_t)ti];
+    D.spill_off = spill_off[(size_t)ti];
+    D.sub_off = sub_off[(size_t)ti];
+    D.pred_off = pred_off[(size_t)ti];
+    D.npred = S.dag_ptr[(size_t)t + 1] - S.dag_ptr[(size_t)t];
+    D.flag_off = flag_off[(size_t)ti];
+    D.id = t;
+    for (int32_t i = 0; i < ns; ++i) spill[(size_t)D.spill_off + i] = sp[i];
+    for (int32_t i = 0; i <= D.nsub; ++i) sub[(size_t)D.sub_off + i] = S.sub_ptr[(size_t)S.tile_sub_ptr[(size_t)t] + i];
+    for (int32_t i = 0; i < D.npred; ++i) pred[(size_t)D.pred_off + i] = S.dag_pred[(size_t)S.dag_ptr[(size_t)t] + i];
+    for (int32_t i = 0; i < T; ++i)
+      if (S.own_first[(size_t)(r0 + i)]) flags[(size_t)D.flag_off + i / 32] |= (1u << (i % 32));
+    int64_t e = 0;
+    int32_t* st = start.data() + D.srow_off + ti;
+    for (int32_t q = 0; q < T; ++q) {
+      const int32_t row = S.srow[(size_t)(r0 + q)];
+      lrow[(size_t)D.srow_off + q] = (uint16_t)(row - r0);
+      st[q] = (int32_t)e;
+      for (int32_t i = S.prow_ptr[(size_t)row]; i < S.prow_ptr[(size_t)row + 1]; ++i) {
+        const int32_t c = S.pcol[(size_t)i];
+        int64_t l;
+        if (c < r1) l = c - r0;
+        else {
+          int32_t lo = 0, hi = ns;
+          while (lo < hi) {
+            int32_t mid = (lo + hi) / 2;
+            if ((int32_t)((uint32_t)sp[mid] & kIdxMask) < c) lo = mid + 1;
+            else hi = mid;
+          }
+          if (lo >= ns || (int32_t)((uint32_t)sp[lo] & kIdxMask) != c) bad |= 1;
+          l = T + lo;
+        }
+        lcol[(size_t)(D.nnz_off + e)] = (uint16_t)l;
+        val[(size_t)(D.nnz_off + e)] = S.pval[(size_t)i];
+        ++e;
+      }
+    }
+    st[T] = (int32_t)e;
+  }
+  if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
+  TileDesc* d_desc;
+  uint16_t *d_lcol, *d_lrow;
+  double* d_val;
+  int32_t *d_start, *d_spill, *d_sub, *d_pred;
+  uint32_t* d_flags;
+  unsigned long long* d_counter;
+  unsigned int* d_done;
+  int rc;
+  if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_lcol, lcol.data(), lcol.size())) ||
+      (rc = upload(P, &d_lrow, lrow.data(), lrow.size())) || (rc = upload(P, &d_val, val.data(), val.size())) ||
+      (rc = upload(P, &d_start, start.data(), start.size())) || (rc = upload(P, &d_spill, spill.data(), spill.size())) ||
+      (rc = upload(P, &d_sub, sub.data(), sub.size())) || (rc = upload(P, &d_pred, pred.data(), pred.size())) ||
+      (rc = upload(P, &d_flags, flags.data(), flags.size())) || (rc = dev_alloc(P, &d_counter, 1)) ||
+      (rc = dev_alloc(P, &d_done, (size_t)std::max(nt, 1))))
+    return rc;
+  cudaMemset(d_counter, 0, sizeof(unsigned long long));
+  cudaMemset(d_done, 0, sizeof(unsigned int) * (size_t)std::max(nt, 1));
+  TiledArgs& A = P->targs;
+  A.tiles = d_desc;
+  A.ntiles = nt;
+  A.lcol = d_lcol;
+  A.val = d_val;
+  A.srow_start = d_start;
+  A.srow_lrow = d_lrow;
+  A.spill = d_spill;
+  A.sub_ptr = d_sub;
+  A.pred = d_pred;
+  A.own_first = d_flags;
+  A.counter = d_counter;
+  A.done = d_done;
+  A.epoch = 0;
+  A.claim_base = 0;
+  A.window_cap = cap;
+  int occ = 0;
+  rc = tiled_max_ctas_per_sm(P->vec, cap, &occ);
+  if (rc) return cuda_fail((cudaError_t)rc, "occupancy query (tiled)");
+  if (occ < 1) return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel does not fit an SM (window cap %d)", cap);
+  P->tiled_grid = std::max(1, std::min(occ * P->sms, nt));
+  P->has_tiled = true;
+  return SYMM_OK;
+}
+
+int build_colored(symmspmv_plan_t* P, const Schedule& S) {
+  const int32_t nt = (int32_t)S.tile_group.size();
+  std::vector<int32_t> ptiles;
+  P->phase_off.assign((size_t)S.n_phases + 1, 0);
+  for (int32_t t = 0; t < nt; ++t) P->phase_off[(size_t)S.tile_phase[(size_t)t] + 1]++;
+  for (int32_t p = 0; p < S.n_phases; ++p) P->phase_off[(size_t)p + 1] += P->phase_off[(size_t)p];
+  ptiles.resize((size_t)nt);
+  std::vector<int32_t> pos(P->phase_off.begin(), P->phase_off.end() - 1);
+  for (int32_t t = 0; t < nt; ++t) ptiles[(size_t)pos[(size_t)S.tile_phase[(size_t)t]]++] = t;
+  int rc;
+  if ((rc = upload(P, &P->d_tile_ptr, S.tile_ptr.data(), S.tile_ptr.size())) ||
+      (rc = upload(P, &P->d_phase_tiles, ptiles.data(), ptiles.size())) ||
+      (rc = upload(P, &P->d_srow, S.srow.data(), S.srow.size())) ||
+      (rc = upload(P, &P->d_tile_sub_ptr, S.tile_sub_ptr.data(), S.tile_sub_ptr.size())) ||
+      (rc = upload(P, &P->d_sub_ptr, S.sub_ptr.data(), S.sub_ptr.size())))
+    return rc;
+  P->has_colored = true;
+  return SYMM_OK;
+}
+
+int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cudaStream_t st) {
+  int rc = 0;
+  P->last_launches = 0;
+  if (P->n == 0) return SYMM_OK;
+  if (variant == SYMM_VARIANT_AUTO) variant = P->variant;
+  if (variant == SYMM_VARIANT_AUTO) variant = P->has_tiled ? SYMM_VARIANT_TILED : SYMM_VARIANT_COLORED;
+  if (variant == SYMM_VARIANT_ATOMIC) {
+    if (!P->has_csr) return set_error(SYMM_ERR_ARG, "variant ATOMIC was not uploaded by this plan");
+    CsrArgs A{P->n, P->d_rp, P->d_col, P->d_val};
+    if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    if ((rc = launch_atomic(A, x, y, P->vec, P->sms, st))) return cuda_fail((cudaError_t)rc, "k_atomic");
+    P->last_launches = 2;
+  } else if (variant == SYMM_VARIANT_COLORED) {
+    if (!P->has_colored) return set_error(SYMM_ERR_ARG, "variant COLORED was not uploaded by this plan");
+    CsrArgs A{P->n, P->d_rp, P->d_col, P->d_val};
+    if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    P->last_launches = 1;
+    for (size_t p = 0; p + 1 < P->phase_off.size(); ++p) {
+      ColoredArgs C{P->d_tile_ptr, P->d_phase_tiles + P->phase_off[p], P->phase_off[p + 1] - P->phase_off[p],
+                    P->d_srow, P->d_tile_sub_ptr, P->d_sub_ptr};
+      if ((rc = launch_colored_phase(A, C, x, y, P->vec, st))) return cuda_fail((cudaError_t)rc, "k_colored");
+      P->last_launches += C.nphase_tiles > 0;
+    }
+  } else if (variant == SYMM_VARIANT_TILED) {
+    if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED was not uploaded by this plan");
+    TiledArgs A = P->targs;
+    A.epoch = P->targs.epoch + 1;
+    if ((rc = launch_tiled(A, x, y, P->vec, P->tiled_grid, st))) return cuda_fail((cudaError_t)rc, "k_tiled");
+    P->targs.epoch = A.epoch;
+    P->targs.claim_base += (unsigned long long)A.ntiles + (unsigned long long)P->tiled_grid;
+    P->last_launches = 1;
+  } else {
+    return set_error(SYMM_ERR_ARG, "unknown variant %d", variant);
+  }
+  return SYMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* symm_status_string(int s) {
+  switch (s) {
+    case SYMM_OK: return "SYMM_OK";
+    case SYMM_ERR_ARG: return "SYMM_ERR_ARG";
+    case SYMM_ERR_NOT_UPPER: return "SYMM_ERR_NOT_UPPER";
+    case SYMM_ERR_UNSORTED: return "SYMM_ERR_UNSORTED";
+    case SYMM_ERR_OVERFLOW: return "SYMM_ERR_OVERFLOW";
+    case SYMM_ERR_OOM: return "SYMM_ERR_OOM";
+    case SYMM_ERR_CUDA: return "SYMM_ERR_CUDA";
+    case SYMM_ERR_NCCL: return "SYMM_ERR_NCCL";
+    case SYMM_ERR_MISMATCH: return "SYMM_ERR_MISMATCH";
+    case SYMM_ERR_ALIAS: return "SYMM_ERR_ALIAS";
+    case SYMM_ERR_SCHEDULE: return "SYMM_ERR_SCHEDULE";
+    case SYMM_ERR_K: return "SYMM_ERR_K";
+    case SYMM_ERR_UNSUPPORTED: return "SYMM_ERR_UNSUPPORTED";
+    default: return "SYMM_ERR_UNKNOWN";
+  }
+}
+const char* symm_last_error(void) { return symm::last_error(); }
+
+void race_config_default(race_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->k = 2;
+  c->n_workers = 0;
+  c->tile_work = 16384;
+  c->balance_by = 1;
+  c->root = -1;
+  c->n_eps = 3;
+  c->eps[0] = 0.8;  // eps_0 = eps_1 = 0.8, eps_{s>1} = 0.5
+  c->eps[1] = 0.8;
+  for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
+  c->max_tile_rows = 4096;
+  c->max_tile_window = 6144;
+  c->reorder = 1;
+  c->validate = 1;
+  c->flags = 0;
+}
+
+int race_build_schedule(const symm_csr_upper* U, const race_config* cfg, race_schedule_t** out) {
+  clear_error();
+  if (!out) return set_error(SYMM_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  std::unique_ptr<race_schedule> s;
+  try {
+    s.reset(new race_schedule());
+    int rc = build_schedule(U, cfg, &s->S);
+    if (rc) return rc;
+  } catch (const std::bad_alloc&) {
+    return set_error(SYMM_ERR_OOM, "host allocation failed while building the schedule");
+  }
+  *out = s.release();
+  return SYMM_OK;
+}
+
+int race_schedule_get_stats(const race_schedule_t* s, race_schedule_stats* o) {
+  if (!s || !o) return set_error(SYMM_ERR_ARG, "NULL argument");
+  const Schedule& S = s->S;
+  std::memset(o, 0, sizeof *o);
+  o->n = S.n;
+  o->total_levels = (int32_t)S.level_ptr.size() - 1;
+  o->n_components = (int32_t)S.roots.size();
+  o->n_groups = (int32_t)S.group_workers.size();
+  o->n_tiles = (int32_t)S.tile_group.size();
+  o->n_phases = S.n_phases;
+  o->max_subcolors = S.max_subcolors;
+  o->max_tile_window = S.max_window;
+  o->max_tile_rows = S.max_rows;
+  o->n_dag_edges = (int32_t)S.dag_pred.size();
+  o->nnz = S.nnz;
+  o->bandwidth_before = S.bw_before;
+  o->bandwidth_after = S.bw_after;
+  o->eta = S.eta;
+  o->build_seconds = S.build_seconds;
+  o->mean_subcolors = S.mean_subcolors;
+  o->spill_entries = (int64_t)S.spill.size();
+  return SYMM_OK;
+}
+
+int race_schedule_permutation(const race_schedule_t* s, int32_t* perm, int32_t* inv) {
+  if (!s) return set_error(SYMM_ERR_ARG, "NULL schedule");
+  if (perm) std::copy(s->S.perm.begin(), s->S.perm.end(), perm);
+  if (inv) std::copy(s->S.inv.begin(), s->S.inv.end(), inv);
+  return SYMM_OK;
+}
+
+int race_schedule_table(const race_schedule_t* s, const char* which, int64_t* len, int32_t* out) {
+  if (!s || !which || !len) return set_error(SYMM_ERR_ARG, "NULL argument");
+  const Schedule& S = s->S;
+  const std::vector<int32_t>* v = nullptr;
+  std::string w(which);
+  if (w == "level_ptr") v = &S.level_ptr;
+  else if (w == "dist") v = &S.dist;
+  else if (w == "roots") v = &S.roots;
+  else if (w == "group_lvl") v = &S.group_lvl;
+  else if (w == "group_workers") v = &S.group_workers;
+  else if (w == "tile_ptr") v = &S.tile_ptr;
+  else if (w == "tile_group") v = &S.tile_group;
+  else if (w == "tile_phase") v = &S.tile_phase;
+  else if (w == "tile_order") v = &S.tile_order;
+  else if (w == "dag_ptr") v = &S.dag_ptr;
+  else if (w == "dag_pred") v = &S.dag_pred;
+  else if (w == "row_subcolor") v = &S.row_subcolor;
+  else if (w == "window_levels") v = &S.windows;
+  else if (w == "srow") v = &S.srow;
+  else if (w == "tile_sub_ptr") v = &S.tile_sub_ptr;
+  else if (w == "sub_ptr") v = &S.sub_ptr;
+  else if (w == "spill") v = &S.spill;
+  else if (w == "own_first") {
+    *len = (int64_t)S.own_first.size();
+    if (out) for (size_t i = 0; i < S.own_first.size(); ++i) out[i] = S.own_first[i];
+    return SYMM_OK;
+  } else if (w == "spill_ptr") {
+    *len = (int64_t)S.spill_ptr.size();
+    if (out) for (size_t i = 0; i < S.spill_ptr.size(); ++i) out[i] = (int32_t)S.spill_ptr[i];
+    return SYMM_OK;
+  }
+  if (!v) return set_error(SYMM_ERR_ARG, "unknown table '%s'", which);
+  *len = (int64_t)v->size();
+  if (out) std::copy(v->begin(), v->end(), out);
+  return SYMM_OK;
+}
+
+int race_schedule_permuted_matrix(const race_schedule_t* s, int32_t* row_ptr, int32_t* col, double* val) {
+  if (!s) return set_error(SYMM_ERR_ARG, "NULL schedule");
+  const Schedule& S = s->S;
+  if (row_ptr) std::copy(S.prow_ptr.begin(), S.prow_ptr.end(), row_ptr);
+  if (col) std::copy(S.pcol.begin(), S.pcol.end(), col);
+  if (val) std::copy(S.pval.begin(), S.pval.end(), val);
+  return SYMM_OK;
+}
+
+void race_schedule_destroy(race_schedule_t* s) { delete s; }
+
+void symmspmv_options_default(symmspmv_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->variant = SYMM_VARIANT_AUTO;
+  o->device = 0;
+  o->vec_order = SYMM_ORDER_PERMUTED;
+  o->nranks = 1;
+  o->rank = 0;
+  o->vec_width = 0;
+  o->ctas_per_sm = 0;
+  o->build_all = 0;
+}
+
+int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symmspmv_options* o,
+                  symmspmv_plan_t** out) {
+  clear_error();
+  if (!s || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  symmspmv_options opt;
+  if (o) opt = *o;
+  else symmspmv_options_default(&opt);
+  const Schedule& S = s->S;
+  if (U && (U->n != S.n || U->nnz != S.nnz))
+    return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
+                     (long long)U->nnz, S.n, (long long)S.nnz);
+  if (opt.variant < 0 || opt.variant > 3) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
+  if (opt.nranks != 1 || opt.rank != 0)
+    return set_error(SYMM_ERR_UNSUPPORTED, "multi-rank plans are driven from Python in this version (nranks=%d)",
+                     opt.nranks);
+  if (opt.vec_width && (opt.vec_width < 1 || opt.vec_width > 32 || (opt.vec_width & (opt.vec_width - 1))))
+    return set_error(SYMM_ERR_ARG, "vec_width %d must be a power of two <= 32", opt.vec_width);
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return set_error(SYMM_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+  }
+  if (opt.device < 0 || opt.device >= ndev) return set_error(SYMM_ERR_ARG, "device %d of %d", opt.device, ndev);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(opt.device);
+  symmspmv_plan_t* P = new symmspmv_plan_t();
+  P->device = opt.device;
+  P->variant = opt.variant;
+  P->vec_order = opt.vec_order;
+  P->n = S.n;
+  P->nnz = S.nnz;
+  P->row_begin = 0;
+  P->row_end = S.n;
+  P->min_bytes = 12 * S.nnz + 4 * ((int64_t)S.n + 1) + 24 * (int64_t)S.n;
+  cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, opt.device);
+  P->vec = opt.vec_width ? opt.vec_width : pick_vec(S.nnz, S.n);
+  int rc = SYMM_OK;
+  const bool all = opt.build_all != 0;
+  const int v = opt.variant;
+  bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_AUTO;
+  bool want_col = all || v == SYMM_VARIANT_COLORED;
+  bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
+  if (want_tiled) {
+    rc = build_tiled(P, S);
+    if (rc == SYMM_ERR_UNSUPPORTED && (v == SYMM_VARIANT_AUTO || all)) {
+      rc = SYMM_OK;  // AUTO falls back to the colored variant
+      want_col = want_csr = true;
+      if (P->variant == SYMM_VARIANT_AUTO) P->variant = SYMM_VARIANT_COLORED;
+    }
+  }
+  if (!rc && want_csr) {
+    if (!(rc = upload(P, &P->d_rp, S.prow_ptr.data(), S.prow_ptr.size())) &&
+        !(rc = upload(P, &P->d_col, S.pcol.data(), S.pcol.size())) &&
+        !(rc = upload(P, &P->d_val, S.pval.data(), S.pval.size())))
+      P->has_csr = true;
+  }
+  if (!rc && want_col) rc = build_colored(P, S);
+  if (!rc) {
+    if (!(rc = upload(P, &P->d_perm, S.perm.data(), S.perm.size())) &&
+        !(rc = upload(P, &P->d_inv, S.inv.data(), S.inv.size())) && !(rc = dev_alloc(P, &P->d_xp, (size_t)S.n)))
+      rc = dev_alloc(P, &P->d_yp, (size_t)S.n);
+  }
+  if (!rc) {
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) rc = cuda_fail(e, "plan upload");
+  }
+  cudaSetDevice(cur);
+  if (rc) {
+    free_plan(P);
+    return rc;
+  }
+  *out = P;
+  return SYMM_OK;
+}
+
+int symmspmv_plan_rows(const symmspmv_plan_t* p, int32_t* b, int32_t* e) {
+  if (!p || !b || !e) return set_error(SYMM_ERR_ARG, "NULL argument");
+  *b = p->row_begin;
+  *e = p->row_end;
+  return SYMM_OK;
+}
+
+int symmspmv_run_variant(symmspmv_plan_t* P, int32_t variant, const double* x, double* y, void* stream) {
+  if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
+  if (P->n > 0 && (!x || !y)) return set_error(SYMM_ERR_ARG, "NULL vector");
+  const uintptr_t xa = (uintptr_t)x, ya = (uintptr_t)y, nb = (uintptr_t)P->n * sizeof(double);
+  if (P->n > 0 && xa < ya + nb && ya < xa + nb) return set_error(SYMM_ERR_ALIAS, "x and y overlap");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != P->device) cudaSetDevice(P->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (P->vec_order == SYMM_ORDER_ORIGINAL) {
+    // x_perm[new] = x[inv[new]];  y[old] = y_perm[perm[old]]
+    int e1 = launch_gather(x, P->d_inv, P->d_xp, P->n, st);
+    if (e1) rc = cuda_fail((cudaError_t)e1, "gather x");
+    else {
+      rc = run_permuted(P, variant < 0 ? SYMM_VARIANT_AUTO : variant, P->d_xp, P->d_yp, st);
+      if (!rc) {
+        int e2 = launch_gather(P->d_yp, P->d_perm, y, P->n, st);
+        if (e2) rc = cuda_fail((cudaError_t)e2, "gather y");
+        P->last_launches += 2;
+      }
+    }
+  } else {
+    rc = run_permuted(P, variant < 0 ? SYMM_VARIANT_AUTO : variant, x, y, st);
+  }
+  if (cur != P->device) cudaSetDevice(cur);
+  return rc;
+}
+
+int symmspmv_run(symmspmv_plan_t* P, const double* x, double* y, void* stream) {
+  return symmspmv_run_variant(P, -1, x, y, stream);
+}
+
+int symmspmv_run_host(symmspmv_plan_t* P, const double* x_host, double* y_host, void* stream) {
+  if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
+  if (P->n == 0) return SYMM_OK;
+  if (!x_host || !y_host) return set_error(SYMM_ERR_ARG, "NULL host vector");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != P->device) cudaSetDevice(P->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t nb = (size_t)P->n * sizeof(double);
+  int rc = SYMM_OK;
+  // d_yp holds x (original order) on the way in; d_xp = permuted x; d_yp = permuted y
+  cudaError_t e = cudaMemcpyAsync(P->d_yp, x_host, nb, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D x");
+  if (!rc) {
+    int e1 = launch_gather(P->d_yp, P->d_inv, P->d_xp, P->n, st);
+    if (e1) rc = cuda_fail((cudaError_t)e1, "gather x");
+  }
+  double* yperm = P->d_yp;
+  if (!rc) rc = run_permuted(P, SYMM_VARIANT_AUTO, P->d_xp, yperm, st);
+  if (!rc) {
+    // y_orig[old] = y_perm[perm[old]] -> written into d_xp (x no longer needed)
+    int e2 = launch_gather(yperm, P->d_perm, P->d_xp, P->n, st);
+    if (e2) rc = cuda_fail((cudaError_t)e2, "gather y");
+    P->last_launches += 2;
+  }
+  if (!rc) {
+    e = cudaMemcpyAsync(y_host, P->d_xp, nb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H y");
+  }
+  if (!rc) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "stream sync");
+  }
+  if (cur != P->device) cudaSetDevice(cur);
+  return rc;
+}
+
+int symmspmv_last_launches(const symmspmv_plan_t* p) { return p ? p->last_launches : 0; }
+
+int symmspmv_plan_bytes(const symmspmv_plan_t* p, int64_t* device_bytes, int64_t* min_bytes) {
+  if (!p) return set_error(SYMM_ERR_ARG, "NULL plan");
+  if (device_bytes) *device_bytes = p->device_bytes;
+  if (min_bytes) *min_bytes = p->min_bytes;
+  return SYMM_OK;
+}
+
+int symmspmv_destroy(symmspmv_plan_t* p) {
+  free_plan(p);
+  return SYMM_OK;
+}
+
+}  // extern "C"

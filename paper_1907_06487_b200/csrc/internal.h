@@ -1,0 +1,132 @@
+// Internal declarations of libsymmspmv.so (product side; never includes or
+// links anything under oracle/).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "symmspmv.h"
+
+namespace symm {
+
+// thread-local error message (symm_last_error)
+int set_error(int code, const char* fmt, ...);
+void clear_error();
+
+// Host-side schedule (race_schedule_t).  Row ids are PERMUTED ids unless a
+// field says "original".
+struct Schedule {
+  int32_t n = 0;
+  int64_t nnz = 0;
+  race_config cfg{};
+  // §4.1 levels and permutation
+  std::vector<int32_t> perm, inv;   // perm[old] = new, inv[new] = old
+  std::vector<int32_t> dist;        // BFS level of every ORIGINAL vertex
+  std::vector<int32_t> roots;       // original id of each island's start
+  std::vector<int32_t> level_ptr;   // [totalLvl+1]
+  // permuted upper CRS U' = upper(P A P^T), rows sorted
+  std::vector<int32_t> prow_ptr, pcol;
+  std::vector<double> pval;
+  // §4.2-4.4.3 level groups
+  std::vector<int32_t> windows;     // (first, end, b) per eps window
+  std::vector<int32_t> group_lvl;   // T_ptr [n_groups+1]
+  std::vector<int32_t> group_workers;
+  // GPU tiles (contiguous row ranges inside level groups)
+  std::vector<int32_t> tile_ptr;    // [n_tiles+1]
+  std::vector<int32_t> tile_group, tile_phase, tile_order;
+  std::vector<int32_t> dag_ptr, dag_pred;  // predecessors of every tile
+  int32_t n_phases = 0;
+  // intra-tile distance-2 row coloring; stored-row order per tile
+  std::vector<int32_t> row_subcolor;  // [n]
+  std::vector<int32_t> srow;          // [n] permuted row ids, per tile sorted by (color,row)
+  std::vector<int32_t> tile_sub_ptr;  // [n_tiles+1] offsets into sub_ptr
+  std::vector<int32_t> sub_ptr;       // per tile (nsub+1) stored-row offsets relative to tile start
+  // per tile sorted unique targets outside its own rows; bit 31 = first writer
+  std::vector<int64_t> spill_ptr;     // [n_tiles+1]
+  std::vector<int32_t> spill;
+  std::vector<uint8_t> own_first;     // [n] tile writes row first (stores, not adds)
+  int32_t max_subcolors = 0, max_window = 0, max_rows = 0;
+  double mean_subcolors = 0.0;
+  int64_t bw_before = 0, bw_after = 0;
+  double eta = 1.0;
+  double build_seconds = 0.0;
+};
+
+// Paper-algorithm building blocks (exposed for white-box tests through
+// race_schedule_table; kept identical in decision order to the cited text).
+std::vector<int32_t> eps_aggregate(const std::vector<int64_t>& level_work, int64_t nthreads, int k,
+                                   double eps);
+int32_t split_window(const std::vector<int64_t>& level_work, int32_t first, int32_t end, int k);
+void alg4_balance(std::vector<int32_t>& T_ptr, const std::vector<int32_t>& worker,
+                  const std::vector<int64_t>& level_work, int kmin);
+
+int build_schedule(const symm_csr_upper* U, const race_config* cfg, Schedule* S);
+
+// ---- device side -----------------------------------------------------------
+constexpr uint32_t kFirstBit = 0x80000000u;
+constexpr uint32_t kIdxMask = 0x7fffffffu;
+
+// One tile of the persistent dataflow kernel (K3).  64 bytes.
+struct TileDesc {
+  int32_t row0;      // first own row (permuted id)
+  int32_t nrows;     // own rows T
+  int32_t nspill;    // targets outside own rows S  (window = T + S)
+  int32_t nsub;      // intra-tile colors
+  int64_t nnz_off;   // first entry in lcol/val (entries of this tile, stored-row order)
+  int32_t srow_off;  // first stored row in srow_start (T + 1 entries) / srow_lrow (T)
+  int32_t spill_off; // first entry in spill list
+  int32_t sub_off;   // first entry in sub_ptr (nsub + 1)
+  int32_t pred_off;  // first entry in pred list
+  int32_t npred;
+  int32_t flag_off;  // first 32-bit word of own-row first-writer bits
+  int32_t id;        // tile id (index into done flags)
+  int32_t pad[3];
+};
+static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
+
+struct TiledArgs {
+  const TileDesc* tiles;     // in claim order
+  int32_t ntiles;
+  const uint16_t* lcol;
+  const double* val;
+  const int32_t* srow_start; // relative entry offsets, T+1 per tile
+  const uint16_t* srow_lrow; // local row id per stored row
+  const int32_t* spill;      // global target id | first bit
+  const int32_t* sub_ptr;    // stored-row offsets per color
+  const int32_t* pred;       // predecessor tile ids
+  const uint32_t* own_first; // bitmask words
+  unsigned long long* counter;  // claim counter (monotone across runs)
+  unsigned int* done;           // per tile id: epoch when flushed
+  unsigned int epoch;
+  unsigned long long claim_base;
+  int32_t window_cap;
+};
+
+struct CsrArgs {
+  int32_t n;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+};
+
+struct ColoredArgs {
+  const int32_t* tile_ptr;     // [n_tiles+1] row ranges (permuted ids)
+  const int32_t* phase_tiles;  // tiles of the phase being launched
+  int32_t nphase_tiles;
+  const int32_t* srow;         // stored rows (global ids), per tile colour-sorted
+  const int32_t* tile_sub_ptr; // offsets into sub_ptr per tile
+  const int32_t* sub_ptr;      // per tile colour pointers, relative to tile row start
+};
+
+// kernel launchers (kernels.cu); return cudaError_t as int
+int launch_zero(double* y, int64_t n, void* stream);
+int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream);
+int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x, double* y, int vec,
+                         void* stream);
+int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, void* stream);
+int tiled_smem_bytes(int window_cap);
+int tiled_max_ctas_per_sm(int vec, int window_cap, int* out);
+int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
+int launch_scatter(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
+
+}  // namespace symm
