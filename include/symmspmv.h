@@ -75,6 +75,7 @@ typedef struct {
   double eps[8];            /* eps_s per stage (0.8, 0.8, 0.5 ...)             */
   int32_t max_tile_rows;    /* hard cap on rows per tile (<= 65535)                          */
   int32_t max_tile_window;  /* cap on |own rows ∪ targets| per tile (smem entries)           */
+  int32_t max_tile_nnz;     /* cap on stored entries per tile (smem staging of the tile)     */
   int32_t reorder;          /* 1 = BFS level permutation; 0 = keep order */
   int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
   uint32_t flags;           /* reserved, 0                                                   */

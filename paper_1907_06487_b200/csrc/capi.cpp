@@ -56,6 +56,7 @@ struct symmspmv_plan {
   bool has_tiled = false;
   TiledArgs targs{};
   int tiled_grid = 0;
+  int tiled_occ = 0;
   // vector order / host staging
   int32_t *d_perm = nullptr, *d_inv = nullptr;
   double *d_xp = nullptr, *d_yp = nullptr;
@@ -112,65 +113,128 @@ int pick_vec(int64_t nnz, int32_t n) {
   return std::max(v, 2);
 }
 
+static inline int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
+
+// K3 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order.
 int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
-  const int32_t nt = (int32_t)S.tile_order.size();
-  const int cap = S.cfg.max_tile_window;
-  if (S.max_window > cap || S.max_window > 65535 || S.max_rows > 65535)
-    return set_error(SYMM_ERR_UNSUPPORTED, "a tile window (%d) exceeds the shared-memory cap (%d)", S.max_window, cap);
+  const int32_t nt = (int32_t)S.tile_group.size();
+  const int32_t n = S.n;
+  std::vector<int32_t> tile_of((size_t)n);
+  for (int32_t t = 0; t < nt; ++t)
+    for (int32_t r = S.tile_ptr[(size_t)t]; r < S.tile_ptr[(size_t)t + 1]; ++r) tile_of[(size_t)r] = t;
   std::vector<TileDesc> desc((size_t)nt);
-  std::vector<int64_t> nnz_off((size_t)nt + 1, 0);
-  std::vector<int32_t> srow_off((size_t)nt + 1, 0), spill_off((size_t)nt + 1, 0), sub_off((size_t)nt + 1, 0),
-      pred_off((size_t)nt + 1, 0), flag_off((size_t)nt + 1, 0);
-  for (int32_t ti = 0; ti < nt; ++ti) {
-    const int32_t t = S.tile_order[(size_t)ti];
-    const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1];
-    nnz_off[(size_t)ti + 1] = nnz_off[(size_t)ti] + (S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0]);
-    srow_off[(size_t)ti + 1] = srow_off[(size_t)ti] + (r1 - r0);
-    spill_off[(size_t)ti + 1] = spill_off[(size_t)ti] + (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
-    sub_off[(size_t)ti + 1] = sub_off[(size_t)ti] + (S.tile_sub_ptr[(size_t)t + 1] - S.tile_sub_ptr[(size_t)t]);
-    pred_off[(size_t)ti + 1] = pred_off[(size_t)ti] + (S.dag_ptr[(size_t)t + 1] - S.dag_ptr[(size_t)t]);
-    flag_off[(size_t)ti + 1] = flag_off[(size_t)ti] + (r1 - r0 + 31) / 32;
-  }
-  std::vector<uint16_t> lcol((size_t)nnz_off[(size_t)nt]), lrow((size_t)srow_off[(size_t)nt]);
-  std::vector<double> val((size_t)nnz_off[(size_t)nt]);
-  std::vector<int32_t> start((size_t)srow_off[(size_t)nt] + (size_t)nt), spill((size_t)spill_off[(size_t)nt]),
-      sub((size_t)sub_off[(size_t)nt]), pred((size_t)pred_off[(size_t)nt]);
-  std::vector<uint32_t> flags((size_t)flag_off[(size_t)nt], 0);
+  std::vector<int64_t> boff((size_t)nt + 1, 0);
+  std::vector<int32_t> ndiag((size_t)nt, 0);
+  int32_t block_cap = 16, window_cap = 1, nnz_cap = 1;
   int bad = 0;
-#pragma omp parallel for schedule(dynamic, 8) reduction(| : bad)
-  for (int32_t ti = 0; ti < nt; ++ti) {
-    const int32_t t = S.tile_order[(size_t)ti];
+  // sizes
+  for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
-    const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
-    const int32_t ns = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
-    TileDesc& D = desc[(size_t)ti];
+    const int32_t S_ = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
+    const int64_t nnz = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
+    int32_t nd = 0;
+    for (int32_t r = r0; r < r1; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
+    ndiag[(size_t)t] = nd;
+    const int64_t W = (int64_t)T + S_;
+    int64_t o_lcol = align16(2 * (int64_t)(T + 1));
+    int64_t o_tidx = align16(o_lcol + 2 * nnz);
+    int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
+    int64_t o_val = align16(o_tptr + 2 * (W + 1));
+    int64_t bytes = align16(o_val + 8 * nnz);
+    if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
+    TileDesc& D = desc[(size_t)t];
     std::memset(&D, 0, sizeof D);
-    D.row0 = r0;
+    D.block_bytes = (int32_t)bytes;
     D.nrows = T;
-    D.nspill = ns;
-    D.nsub = S.tile_sub_ptr[(size_t)t + 1] - S.tile_sub_ptr[(size_t)t] - 1;
-    D.nnz_off = nnz_off[(size_t)ti];
-    D.srow_off = srow_off[(size_t)ti];
-    D.spill_off = spill_off[(size_t)ti];
-    D.sub_off = sub_off[(size_t)ti];
-    D.pred_off = pred_off[(size_t)ti];
-    D.npred = S.dag_ptr[(size_t)t + 1] - S.dag_ptr[(size_t)t];
-    D.flag_off = flag_off[(size_t)ti];
-    D.id = t;
-    for (int32_t i = 0; i < ns; ++i) spill[(size_t)D.spill_off + i] = sp[i];
-    for (int32_t i = 0; i <= D.nsub; ++i) sub[(size_t)D.sub_off + i] = S.sub_ptr[(size_t)S.tile_sub_ptr[(size_t)t] + i];
-    for (int32_t i = 0; i < D.npred; ++i) pred[(size_t)D.pred_off + i] = S.dag_pred[(size_t)S.dag_ptr[(size_t)t] + i];
-    for (int32_t i = 0; i < T; ++i)
-      if (S.own_first[(size_t)(r0 + i)]) flags[(size_t)D.flag_off + i / 32] |= (1u << (i % 32));
-    int64_t e = 0;
-    int32_t* st = start.data() + D.srow_off + ti;
-    for (int32_t q = 0; q < T; ++q) {
-      const int32_t row = S.srow[(size_t)(r0 + q)];
-      lrow[(size_t)D.srow_off + q] = (uint16_t)(row - r0);
-      st[q] = (int32_t)e;
-      for (int32_t i = S.prow_ptr[(size_t)row]; i < S.prow_ptr[(size_t)row + 1]; ++i) {
+    D.nspill = S_;
+    D.nnz = (int32_t)nnz;
+    D.row0 = r0;
+    D.o_lcol = (uint16_t)o_lcol;
+    D.o_tidx = (uint16_t)o_tidx;
+    D.o_tptr = (uint16_t)o_tptr;
+    D.o_val = (uint16_t)o_val;
+    boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
+    D.block_off = boff[(size_t)t];
+    D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
+    D.in_off = r0 + t;  // T+1 pointers per tile
+    block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
+    window_cap = std::max<int32_t>(window_cap, (int32_t)W);
+    nnz_cap = std::max<int32_t>(nnz_cap, (int32_t)nnz);
+  }
+  if (bad)
+    return set_error(SYMM_ERR_UNSUPPORTED, "tile %d does not fit the 64 KB tile-block format (use smaller tiles)", bad - 1);
+  // incoming contributions: (owner tile, local target, writer, spill index) -> slot
+  const int64_t nsp = (int64_t)S.spill.size();
+  std::vector<I2> pairs((size_t)nsp);
+  std::vector<int64_t> own_cnt((size_t)nt + 1, 0);
+  for (int64_t q = 0; q < nsp; ++q) own_cnt[(size_t)tile_of[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)] + 1]++;
+  for (int32_t t = 0; t < nt; ++t) own_cnt[(size_t)t + 1] += own_cnt[(size_t)t];
+  std::vector<int64_t> order((size_t)nsp);  // spill entry ids grouped by owner, writer-ascending
+  {
+    std::vector<int64_t> pos(own_cnt.begin(), own_cnt.end() - 1);
+    for (int64_t q = 0; q < nsp; ++q) order[(size_t)pos[(size_t)tile_of[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)]]++] = q;
+  }
+  std::vector<int32_t> in_ptr((size_t)n + (size_t)nt, 0);
+  std::vector<std::vector<int32_t>> wr((size_t)nt);
+  std::vector<int32_t> spill_writer((size_t)nsp);
+  for (int32_t w = 0; w < nt; ++w)
+    for (int64_t q = S.spill_ptr[(size_t)w]; q < S.spill_ptr[(size_t)w + 1]; ++q) spill_writer[(size_t)q] = w;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int32_t t = 0; t < nt; ++t) {
+    const int32_t r0 = S.tile_ptr[(size_t)t], T = S.tile_ptr[(size_t)t + 1] - r0;
+    const int64_t b0 = own_cnt[(size_t)t], b1 = own_cnt[(size_t)t + 1];
+    // stable sort by target (writer order inside one target is preserved)
+    std::stable_sort(order.begin() + b0, order.begin() + b1, [&](int64_t a, int64_t b) {
+      return ((uint32_t)S.spill[(size_t)a] & kIdxMask) < ((uint32_t)S.spill[(size_t)b] & kIdxMask);
+    });
+    int32_t* ip = in_ptr.data() + r0 + t;
+    std::vector<int32_t> cnt((size_t)T + 1, 0);
+    for (int64_t k = b0; k < b1; ++k) {
+      const int64_t q = order[(size_t)k];
+      const int32_t c = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
+      cnt[(size_t)(c - r0) + 1]++;
+      pairs[(size_t)q] = I2{c, (int32_t)k};  // slot k: contiguous per owner
+      wr[(size_t)t].push_back(spill_writer[(size_t)q]);
+    }
+    for (int32_t i = 0; i < T; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
+    for (int32_t i = 0; i <= T; ++i) ip[i] = cnt[(size_t)i];
+    auto& v = wr[(size_t)t];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    desc[(size_t)t].in_base = (int32_t)b0;
+  }
+  std::vector<int32_t> writers;
+  for (int32_t t = 0; t < nt; ++t) {
+    desc[(size_t)t].wr_off = (int32_t)writers.size();
+    desc[(size_t)t].nwr = (int32_t)wr[(size_t)t].size();
+    for (int32_t w : wr[(size_t)t]) {
+      if (w >= t) bad = 1;  // writers must precede owners in claim order
+      writers.push_back(w);
+    }
+  }
+  if (bad) return set_error(SYMM_ERR_SCHEDULE, "a writer tile does not precede its owner");
+  { std::vector<std::vector<int32_t>>().swap(wr); }
+  // tile blocks
+  std::vector<unsigned char> blocks((size_t)boff[(size_t)nt], 0);
+#pragma omp parallel for schedule(dynamic, 8) reduction(| : bad)
+  for (int32_t t = 0; t < nt; ++t) {
+    const TileDesc& D = desc[(size_t)t];
+    const int32_t r0 = D.row0, T = D.nrows, r1 = r0 + T, ns = D.nspill, W = T + ns;
+    const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
+    unsigned char* blk = blocks.data() + D.block_off;
+    uint16_t* start = reinterpret_cast<uint16_t*>(blk);
+    uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
+    uint16_t* tidx = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
+    uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
+    double* val = reinterpret_cast<double*>(blk + D.o_val);
+    const int32_t e0 = S.prow_ptr[(size_t)r0];
+    std::vector<int32_t> tcnt((size_t)W + 1, 0);
+    for (int32_t r = r0; r < r1; ++r) {
+      start[r - r0] = (uint16_t)(S.prow_ptr[(size_t)r] - e0);
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
         const int32_t c = S.pcol[(size_t)i];
-        int64_t l;
+        int32_t l;
         if (c < r1) l = c - r0;
         else {
           int32_t lo = 0, hi = ns;
@@ -182,51 +246,56 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
           if (lo >= ns || (int32_t)((uint32_t)sp[lo] & kIdxMask) != c) bad |= 1;
           l = T + lo;
         }
-        lcol[(size_t)(D.nnz_off + e)] = (uint16_t)l;
-        val[(size_t)(D.nnz_off + e)] = S.pval[(size_t)i];
-        ++e;
+        lcol[i - e0] = (uint16_t)l;
+        val[i - e0] = S.pval[(size_t)i];
+        if (c != r) tcnt[(size_t)l + 1]++;
       }
     }
-    st[T] = (int32_t)e;
+    start[T] = (uint16_t)(S.prow_ptr[(size_t)r1] - e0);
+    for (int32_t l = 0; l < W; ++l) tcnt[(size_t)l + 1] += tcnt[(size_t)l];
+    for (int32_t l = 0; l <= W; ++l) tptr[l] = (uint16_t)tcnt[(size_t)l];
+    for (int32_t r = r0; r < r1; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
+        if (S.pcol[(size_t)i] != r) tidx[tcnt[lcol[i - e0]]++] = (uint16_t)(i - e0);
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   TileDesc* d_desc;
-  uint16_t *d_lcol, *d_lrow;
-  double* d_val;
-  int32_t *d_start, *d_spill, *d_sub, *d_pred;
-  uint32_t* d_flags;
+  unsigned char* d_blocks;
+  I2* d_pairs;
+  int32_t *d_inptr, *d_writers;
+  double* d_spill;
   unsigned long long* d_counter;
-  unsigned int* d_done;
+  unsigned int* d_ready;
   int rc;
-  if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_lcol, lcol.data(), lcol.size())) ||
-      (rc = upload(P, &d_lrow, lrow.data(), lrow.size())) || (rc = upload(P, &d_val, val.data(), val.size())) ||
-      (rc = upload(P, &d_start, start.data(), start.size())) || (rc = upload(P, &d_spill, spill.data(), spill.size())) ||
-      (rc = upload(P, &d_sub, sub.data(), sub.size())) || (rc = upload(P, &d_pred, pred.data(), pred.size())) ||
-      (rc = upload(P, &d_flags, flags.data(), flags.size())) || (rc = dev_alloc(P, &d_counter, 1)) ||
-      (rc = dev_alloc(P, &d_done, (size_t)std::max(nt, 1))))
+  if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
+      (rc = upload(P, &d_pairs, pairs.data(), pairs.size())) || (rc = upload(P, &d_inptr, in_ptr.data(), in_ptr.size())) ||
+      (rc = upload(P, &d_writers, writers.data(), writers.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)) ||
+      (rc = dev_alloc(P, &d_counter, 1)) || (rc = dev_alloc(P, &d_ready, (size_t)std::max(nt, 1))))
     return rc;
   cudaMemset(d_counter, 0, sizeof(unsigned long long));
-  cudaMemset(d_done, 0, sizeof(unsigned int) * (size_t)std::max(nt, 1));
+  cudaMemset(d_ready, 0, sizeof(unsigned int) * (size_t)std::max(nt, 1));
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
   A.ntiles = nt;
-  A.lcol = d_lcol;
-  A.val = d_val;
-  A.srow_start = d_start;
-  A.srow_lrow = d_lrow;
-  A.spill = d_spill;
-  A.sub_ptr = d_sub;
-  A.pred = d_pred;
-  A.own_first = d_flags;
-  A.counter = d_counter;
-  A.done = d_done;
+  A.blocks = d_blocks;
+  A.pairs = d_pairs;
+  A.in_ptr = d_inptr;
+  A.writers = d_writers;
+  A.spill_buf = d_spill;
+  A.ready = d_ready;
   A.epoch = 0;
+  A.counter = d_counter;
   A.claim_base = 0;
-  A.window_cap = cap;
+  A.block_cap = block_cap;
+  A.window_cap = window_cap;
+  A.nnz_cap = nnz_cap;
+  if (tiled_smem_bytes(A) > 227 * 1024)
+    return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel needs %d B of shared memory", tiled_smem_bytes(A));
   int occ = 0;
-  rc = tiled_max_ctas_per_sm(P->vec, cap, &occ);
+  rc = tiled_max_ctas_per_sm(P->vec, A, &occ);
   if (rc) return cuda_fail((cudaError_t)rc, "occupancy query (tiled)");
-  if (occ < 1) return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel does not fit an SM (window cap %d)", cap);
+  if (occ < 1) return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel does not fit an SM");
+  P->tiled_occ = occ;
   P->tiled_grid = std::max(1, std::min(occ * P->sms, nt));
   P->has_tiled = true;
   return SYMM_OK;
@@ -318,15 +387,16 @@ void race_config_default(race_config* c) {
   std::memset(c, 0, sizeof *c);
   c->k = 2;
   c->n_workers = 0;
-  c->tile_work = 16384;
+  c->tile_work = 4608;
   c->balance_by = 1;
   c->root = -1;
   c->n_eps = 3;
   c->eps[0] = 0.8;  // eps_0 = eps_1 = 0.8, eps_{s>1} = 0.5
   c->eps[1] = 0.8;
   for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
-  c->max_tile_rows = 4096;
-  c->max_tile_window = 6144;
+  c->max_tile_rows = 2048;
+  c->max_tile_window = 2048;
+  c->max_tile_nnz = 4096;
   c->reorder = 1;
   c->validate = 1;
   c->flags = 0;

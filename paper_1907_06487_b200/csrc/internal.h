@@ -63,43 +63,49 @@ void alg4_balance(std::vector<int32_t>& T_ptr, const std::vector<int32_t>& worke
 int build_schedule(const symm_csr_upper* U, const race_config* cfg, Schedule* S);
 
 // ---- device side -----------------------------------------------------------
+struct alignas(8) I2 {
+  int32_t x, y;
+};
+
 constexpr uint32_t kFirstBit = 0x80000000u;
 constexpr uint32_t kIdxMask = 0x7fffffffu;
 
-// One tile of the persistent dataflow kernel (K3).  64 bytes.
+// One tile of the persistent owner-computes kernel (K3).  64 bytes.
+// The tile's block (bulk-copied to shared memory) holds, 16-B aligned:
+//   start u16[T+1] | lcol u16[nnz] | tidx u16[noff] | tptr u16[W+1] | val f64[nnz]
+// start: entry offsets of the T own rows (natural row order); lcol: local
+// column (own rows 0..T-1, then spill targets T..W-1); tidx/tptr: the
+// off-diagonal entries grouped by local target (CSC of the tile).
 struct TileDesc {
-  int32_t row0;      // first own row (permuted id)
-  int32_t nrows;     // own rows T
-  int32_t nspill;    // targets outside own rows S  (window = T + S)
-  int32_t nsub;      // intra-tile colors
-  int64_t nnz_off;   // first entry in lcol/val (entries of this tile, stored-row order)
-  int32_t srow_off;  // first stored row in srow_start (T + 1 entries) / srow_lrow (T)
-  int32_t spill_off; // first entry in spill list
-  int32_t sub_off;   // first entry in sub_ptr (nsub + 1)
-  int32_t pred_off;  // first entry in pred list
-  int32_t npred;
-  int32_t flag_off;  // first 32-bit word of own-row first-writer bits
-  int32_t id;        // tile id (index into done flags)
-  int32_t pad[3];
+  int64_t block_off;    // byte offset of the block
+  int32_t block_bytes;  // multiple of 16, < 65536
+  int32_t nrows;        // T
+  int32_t nspill;       // S (window W = T + S)
+  int32_t nnz;          // stored entries of the tile
+  int32_t row0;         // first own row (permuted id)
+  int32_t spill_off;    // first (target, slot) pair of this tile
+  int32_t in_off;       // first of the T+1 incoming pointers of this tile
+  int32_t in_base;      // first incoming slot in spill_buf
+  int32_t nwr;          // writer tiles this tile waits for
+  int32_t wr_off;       // first writer id
+  uint16_t o_lcol, o_tidx, o_tptr, o_val;  // byte offsets inside the block
+  int32_t pad;
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
 
 struct TiledArgs {
-  const TileDesc* tiles;     // in claim order
+  const TileDesc* tiles;          // tile id order (= BFS order = claim order)
   int32_t ntiles;
-  const uint16_t* lcol;
-  const double* val;
-  const int32_t* srow_start; // relative entry offsets, T+1 per tile
-  const uint16_t* srow_lrow; // local row id per stored row
-  const int32_t* spill;      // global target id | first bit
-  const int32_t* sub_ptr;    // stored-row offsets per color
-  const int32_t* pred;       // predecessor tile ids
-  const uint32_t* own_first; // bitmask words
-  unsigned long long* counter;  // claim counter (monotone across runs)
-  unsigned int* done;           // per tile id: epoch when flushed
+  const unsigned char* blocks;
+  const I2* pairs;                // per spill entry: (global target, incoming slot)
+  const int32_t* in_ptr;          // per tile T+1 incoming offsets (relative to in_base)
+  const int32_t* writers;         // writer tile ids per tile
+  double* spill_buf;              // staged contributions to other tiles' rows
+  unsigned int* ready;            // per tile: epoch when its spill contributions are staged
   unsigned int epoch;
+  unsigned long long* counter;    // claim counter (monotone across runs)
   unsigned long long claim_base;
-  int32_t window_cap;
+  int32_t block_cap, window_cap, nnz_cap;
 };
 
 struct CsrArgs {
@@ -124,8 +130,8 @@ int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms
 int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x, double* y, int vec,
                          void* stream);
 int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, void* stream);
-int tiled_smem_bytes(int window_cap);
-int tiled_max_ctas_per_sm(int vec, int window_cap, int* out);
+int tiled_smem_bytes(const TiledArgs& T);
+int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 int launch_scatter(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 

@@ -6,12 +6,10 @@
 //  K2 k_colored    one launch per phase (tiles of one colour); inside a tile the
 //                  rows of one intra-tile colour are write-disjoint -> plain
 //                  read-modify-write of y in L2, __syncthreads between colours.
-//  K3 k_tiled      persistent dataflow kernel: each CTA claims tiles in a
-//                  topological order, stages x of the tile's window (own rows +
-//                  targets) in shared memory, accumulates y in shared memory
-//                  colour by colour, then waits for its predecessor tiles
-//                  (RACE's local synchronisation) and
-//                  flushes the window to y in a fixed order -> deterministic.
+//  K3 k_tiled      persistent owner-computes kernel: TMA bulk copies of whole
+//                  tile blocks into double-buffered smem, two conflict-free smem
+//                  passes, staged cross-tile contributions with depth-1
+//                  dependencies -> deterministic, y written once (see below).
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -144,90 +142,154 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
   }
 }
 
-// ---------------------------------------------------------------- K3 tiled dataflow
+// ---------------------------------------------------------------- K3 tiled (owner computes)
+// Per tile (one CTA at a time, persistent grid, tiles claimed in BFS order):
+//   1. the whole tile block (matrix entries + CSC of the tile) arrives by one
+//      cp.async.bulk (TMA) into a double-buffered smem slot; the NEXT tile's
+//      block is already in flight while this one is computed;
+//   2. x of the tile window (own rows + spill targets) is gathered to smem;
+//   3. pass 1 (rows):    ys[i] = sum_e a_e x[c_e]          (tmp)
+//                        P[e]  = a_e x[i] for off-diagonal e
+//      pass 2 (targets): ys[l] += sum_{e: c_e = l} P[e]  (b[col] += ...)
+//      both passes are conflict-free and in a fixed order -> deterministic;
+//   4. contributions to rows of later tiles (spill) are staged in spill_buf,
+//      then the tile publishes `ready`;
+//   5. the owner of a row waits only for the tiles that wrote into its rows
+//      (all earlier in claim order, none of them waits before publishing:
+//      dependency depth 1, RACE's "local synchronisation"),
+//      adds their staged contributions in slot order and stores y once.
+// y is written exactly once per row: no pre-zeroing, no atomics.
 constexpr int kTiledThreads = 512;
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void issue_tile(const TiledArgs& A, long long t, unsigned char* buf, uint64_t* bar) {
+  const TileDesc& D = A.tiles[t];
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, (unsigned)D.block_bytes);
+  bulk_g2s(buf, A.blocks + D.block_off, (unsigned)D.block_bytes, bar);
+}
+
 template <int V>
-__global__ void __launch_bounds__(kTiledThreads, 2) k_tiled(TiledArgs A, const double* __restrict__ x,
-                                                            double* __restrict__ y) {
-  extern __shared__ double smem[];
-  double* xs = smem;
-  double* ys = smem + A.window_cap;
-  __shared__ long long s_claim;
+__global__ void __launch_bounds__(kTiledThreads) k_tiled(TiledArgs A, const double* __restrict__ x,
+                                                         double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ long long s_next;
+  unsigned char* buf0 = sm;
+  unsigned char* buf1 = sm + A.block_cap;
+  double* xs = reinterpret_cast<double*>(sm + 2 * (size_t)A.block_cap);
+  double* ys = xs + A.window_cap;
+  double* Pp = ys + A.window_cap;
   constexpr int RPW = 32 / V;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int sub = lane % V;
-  const int wid = tid >> 5;
   constexpr int NW = kTiledThreads / 32;
-  unsigned long long* counter = A.counter;
-  for (;;) {
-    if (tid == 0) s_claim = (long long)(atomicAdd(counter, 1ull) - A.claim_base);
-    __syncthreads();
-    const long long ti = s_claim;
-    if (ti >= A.ntiles) break;
-    const TileDesc D = A.tiles[ti];
-    const int T = D.nrows, S = D.nspill;
-    const int32_t* spill = A.spill + D.spill_off;
-    // stage the window of x; clear the window of y
-    for (int i = tid; i < T; i += kTiledThreads) {
-      xs[i] = x[D.row0 + i];
-      ys[i] = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, sub = lane % V, wid = tid >> 5;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    long long t = (long long)(atomicAdd(A.counter, 1ull) - A.claim_base);
+    s_next = t;
+    if (t < A.ntiles) issue_tile(A, t, buf0, &mbar[0]);
+  }
+  __syncthreads();
+  long long cur = s_next;
+  int b = 0;
+  unsigned par0 = 0, par1 = 0;
+  while (cur < A.ntiles) {
+    __syncthreads();  // every thread has read s_next
+    if (tid == 0) {
+      long long t = (long long)(atomicAdd(A.counter, 1ull) - A.claim_base);
+      s_next = t;
+      if (t < A.ntiles) issue_tile(A, t, b ? buf0 : buf1, b ? &mbar[0] : &mbar[1]);
     }
-    for (int i = tid; i < S; i += kTiledThreads) {
-      xs[T + i] = x[(uint32_t)spill[i] & kIdxMask];
-      ys[T + i] = 0.0;
-    }
+    const TileDesc D = A.tiles[cur];
+    const int T = D.nrows, S = D.nspill, W = T + S;
+    const I2* pairs = A.pairs + D.spill_off;
+    for (int i = tid; i < T; i += kTiledThreads) xs[i] = x[D.row0 + i];
+    for (int i = tid; i < S; i += kTiledThreads) xs[T + i] = __ldg(x + pairs[i].x);
+    unsigned char* blk = b ? buf1 : buf0;
+    if (b) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
+    else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
     __syncthreads();
-    const int* sp = A.sub_ptr + D.sub_off;
-    const int32_t* start = A.srow_start + D.srow_off + ti;  // T+1 entries per tile
-    const uint16_t* lrow = A.srow_lrow + D.srow_off;
-    const uint16_t* lcol = A.lcol + D.nnz_off;
-    const double* val = A.val + D.nnz_off;
-    for (int s = 0; s < D.nsub; ++s) {
-      const int qa = sp[s], qb = sp[s + 1];
-      for (int base = qa + wid * RPW; base < qb; base += NW * RPW) {
-        const int q = base + lane / V;
-        const bool valid = q < qb;
-        double sum = 0.0;
-        int lr = 0;
-        if (valid) {
-          lr = lrow[q];
-          const int eb = start[q], ee = start[q + 1];
-          const double xr = xs[lr];
-          for (int e = eb + sub; e < ee; e += V) {
-            const int lc = ld_stream_u16(lcol + e);
-            const double a = ld_stream_f64(val + e);
-            sum += a * xs[lc];
-            if (lc != lr) ys[lc] += a * xr;  // write-disjoint inside the colour
-          }
+    const uint16_t* start = reinterpret_cast<const uint16_t*>(blk);
+    const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
+    const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
+    const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
+    const double* val = reinterpret_cast<const double*>(blk + D.o_val);
+    // pass 1: rows (V lanes per row)
+    for (int base = wid * RPW; base < T; base += NW * RPW) {
+      const int i = base + lane / V;
+      double sum = 0.0;
+      if (i < T) {
+        const int eb = start[i], ee = start[i + 1];
+        const double xi = xs[i];
+        for (int e = eb + sub; e < ee; e += V) {
+          const int c = lcol[e];
+          const double a = val[e];
+          sum += a * xs[c];
+          if (c != i) Pp[e] = a * xi;
         }
-        sum = group_sum<V>(sum);
-        if (valid && sub == 0) ys[lr] += sum;
       }
-      __syncthreads();
+      sum = group_sum<V>(sum);
+      if (i < T && sub == 0) ys[i] = sum;
     }
-    // local synchronisation: wait until every conflicting earlier-phase tile flushed
-    for (int i = tid; i < D.npred; i += kTiledThreads) {
-      const unsigned int* f = A.done + A.pred[D.pred_off + i];
-      while (ld_acquire_u32(f) != A.epoch) __nanosleep(64);
+    __syncthreads();
+    // pass 2: targets (one thread per local target, entries in stored order)
+    for (int l = tid; l < W; l += kTiledThreads) {
+      double acc = l < T ? ys[l] : 0.0;
+      const int jb = tptr[l], je = tptr[l + 1];
+      for (int j = jb; j < je; ++j) acc += Pp[tidx[j]];
+      ys[l] = acc;
+    }
+    __syncthreads();
+    // stage contributions to later tiles' rows, then publish
+    for (int i = tid; i < S; i += kTiledThreads) __stcg(A.spill_buf + pairs[i].y, ys[T + i]);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release_u32(A.ready + cur, A.epoch);
+    // wait for the writers of this tile's rows (all claimed earlier)
+    for (int k = tid; k < D.nwr; k += kTiledThreads) {
+      const unsigned int* f = A.ready + A.writers[D.wr_off + k];
+      while (ld_acquire_u32(f) != A.epoch) __nanosleep(32);
       __threadfence();
     }
     __syncthreads();
-    const uint32_t* ownf = A.own_first + D.flag_off;
+    const int32_t* ip = A.in_ptr + D.in_off;
+    const double* inb = A.spill_buf + D.in_base;
     for (int i = tid; i < T; i += kTiledThreads) {
-      const bool first = (ownf[i >> 5] >> (i & 31)) & 1u;
-      double* p = y + D.row0 + i;
-      __stcg(p, first ? ys[i] : __ldcg(p) + ys[i]);
+      double acc = ys[i];
+      const int jb = ip[i], je = ip[i + 1];
+      for (int j = jb; j < je; ++j) acc += __ldcg(inb + j);
+      y[D.row0 + i] = acc;
     }
-    for (int i = tid; i < S; i += kTiledThreads) {
-      const uint32_t e = (uint32_t)spill[i];
-      double* p = y + (e & kIdxMask);
-      __stcg(p, (e & kFirstBit) ? ys[T + i] : __ldcg(p) + ys[T + i]);
-    }
-    __threadfence();
     __syncthreads();
-    if (tid == 0) st_release_u32(A.done + D.id, A.epoch);
+    cur = s_next;
+    b ^= 1;
   }
 }
 
@@ -291,22 +353,23 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
   return (int)cudaGetLastError();
 }
 
-int tiled_smem_bytes(int window_cap) { return 2 * window_cap * (int)sizeof(double); }
+int tiled_smem_bytes(const TiledArgs& T) {
+  return 2 * T.block_cap + 2 * T.window_cap * 8 + T.nnz_cap * 8;
+}
 
 template <int V>
 static int tiled_setup(int smem) {
   return (int)cudaFuncSetAttribute(k_tiled<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-int tiled_max_ctas_per_sm(int vec, int window_cap, int* out) {
-  const int smem = tiled_smem_bytes(window_cap);
+int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out) {
+  const int smem = tiled_smem_bytes(T);
   int rc = 0, occ = 0;
   switch (vec) {
-#define OCC(VV)                                                                             \
-  case VV:                                                                                  \
-    rc = tiled_setup<VV>(smem);                                                             \
-    if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<VV>,     \
-                                                                     kTiledThreads, smem);  \
+#define OCC(VV)                                                                                                \
+  case VV:                                                                                                     \
+    rc = tiled_setup<VV>(smem);                                                                                \
+    if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<VV>, kTiledThreads, smem); \
     break;
     OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
@@ -319,7 +382,7 @@ int tiled_max_ctas_per_sm(int vec, int window_cap, int* out) {
 int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, void* stream) {
   if (T.ntiles <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  const int smem = tiled_smem_bytes(T.window_cap);
+  const int smem = tiled_smem_bytes(T);
   switch (vec) {
     case 1: k_tiled<1><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
     case 2: k_tiled<2><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;

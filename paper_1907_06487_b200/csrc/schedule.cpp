@@ -351,7 +351,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   else race_config_default(&cfg);
   if (cfg.k < 2) return set_error(SYMM_ERR_K, "distance k = %d < 2: SymmSpMV needs distance-2 (PAPER.md:787-789)", cfg.k);
   if (cfg.tile_work <= 0 || cfg.max_tile_rows <= 0 || cfg.max_tile_rows > 65535 || cfg.max_tile_window < 64 ||
-      cfg.max_tile_window > 65535 || cfg.n_eps < 1 || cfg.n_eps > 8 || cfg.n_workers < 0)
+      cfg.max_tile_window > 65535 || cfg.max_tile_nnz < 1 || cfg.max_tile_nnz > 65535 || cfg.n_eps < 1 || cfg.n_eps > 8 || cfg.n_workers < 0)
     return set_error(SYMM_ERR_ARG, "invalid race_config field");
   int rc = validate_upper(U);
   if (rc) return rc;
@@ -541,7 +541,8 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
           auto rg = st.back();
           st.pop_back();
           int32_t nr = rg.second - rg.first;
-          bool fits = nr <= cfg.max_tile_rows && window_of(rg.first, rg.second) <= cfg.max_tile_window;
+          bool fits = nr <= cfg.max_tile_rows && (rp[rg.second] - rp[rg.first]) <= cfg.max_tile_nnz &&
+                      window_of(rg.first, rg.second) <= cfg.max_tile_window;
           if (fits || nr == 1) { done.push_back(rg); continue; }
           int32_t mid = rg.first + nr / 2;
           st.push_back({mid, rg.second});
