@@ -42,6 +42,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-variants", action="store_true", help="also time the other variants (extra key)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--tile-nnz", type=int, default=0, help="race_config.max_tile_nnz override")
+    ap.add_argument("--tile-window", type=int, default=0, help="race_config.max_tile_window override")
+    ap.add_argument("--tile-work", type=int, default=0, help="race_config.tile_work override")
+    ap.add_argument("--vec", type=int, default=0, help="lanes per row override")
     return ap.parse_args()
 
 
@@ -211,12 +215,21 @@ def main():
     t_gen = time.perf_counter() - t0
     nf = nnz_full_of(U)
     t0 = time.perf_counter()
-    s = P.build_schedule(U)
+    sched_kw = {}
+    if a.tile_nnz:
+        sched_kw["max_tile_nnz"] = a.tile_nnz
+    if a.tile_window:
+        sched_kw["max_tile_window"] = a.tile_window
+        sched_kw["max_tile_rows"] = a.tile_window
+    if a.tile_work:
+        sched_kw["tile_work"] = a.tile_work
+    s = P.build_schedule(U, **sched_kw)
     t_sched = time.perf_counter() - t0
     st = s.stats
     perm, inv = s.permutation()
     t0 = time.perf_counter()
-    plan = P.Plan(s, U, variant=a.variant if not a.all_variants else "auto", build_all=a.all_variants)
+    plan = P.Plan(s, U, variant=a.variant if not a.all_variants else "auto", build_all=a.all_variants,
+                  vec_width=a.vec)
     t_plan = time.perf_counter() - t0
     dev_bytes, bytes_min = plan.bytes()
     n = U.n

@@ -140,7 +140,9 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     int64_t o_lcol = align16(2 * (int64_t)(T + 1));
     int64_t o_tidx = align16(o_lcol + 2 * nnz);
     int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
-    int64_t o_val = align16(o_tptr + 2 * (W + 1));
+    int64_t o_inptr = align16(o_tptr + 2 * (W + 1));
+    int64_t o_slot = align16(o_inptr + 2 * (int64_t)(T + 1));
+    int64_t o_val = align16(o_slot + 4 * (int64_t)S_);
     int64_t bytes = align16(o_val + 8 * nnz);
     if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
     TileDesc& D = desc[(size_t)t];
@@ -153,11 +155,12 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     D.o_lcol = (uint16_t)o_lcol;
     D.o_tidx = (uint16_t)o_tidx;
     D.o_tptr = (uint16_t)o_tptr;
+    D.o_inptr = (uint16_t)o_inptr;
+    D.o_slot = (uint16_t)o_slot;
     D.o_val = (uint16_t)o_val;
     boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
     D.block_off = boff[(size_t)t];
     D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
-    D.in_off = r0 + t;  // T+1 pointers per tile
     block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
     window_cap = std::max<int32_t>(window_cap, (int32_t)W);
     nnz_cap = std::max<int32_t>(nnz_cap, (int32_t)nnz);
@@ -166,7 +169,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     return set_error(SYMM_ERR_UNSUPPORTED, "tile %d does not fit the 64 KB tile-block format (use smaller tiles)", bad - 1);
   // incoming contributions: (owner tile, local target, writer, spill index) -> slot
   const int64_t nsp = (int64_t)S.spill.size();
-  std::vector<I2> pairs((size_t)nsp);
+  std::vector<int32_t> targets((size_t)nsp), slots((size_t)nsp);
   std::vector<int64_t> own_cnt((size_t)nt + 1, 0);
   for (int64_t q = 0; q < nsp; ++q) own_cnt[(size_t)tile_of[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)] + 1]++;
   for (int32_t t = 0; t < nt; ++t) own_cnt[(size_t)t + 1] += own_cnt[(size_t)t];
@@ -175,7 +178,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     std::vector<int64_t> pos(own_cnt.begin(), own_cnt.end() - 1);
     for (int64_t q = 0; q < nsp; ++q) order[(size_t)pos[(size_t)tile_of[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)]]++] = q;
   }
-  std::vector<int32_t> in_ptr((size_t)n + (size_t)nt, 0);
+  std::vector<int32_t> in_ptr((size_t)n + (size_t)nt, 0);  // T+1 per tile at row0 + t
   std::vector<std::vector<int32_t>> wr((size_t)nt);
   std::vector<int32_t> spill_writer((size_t)nsp);
   for (int32_t w = 0; w < nt; ++w)
@@ -194,11 +197,13 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
       const int64_t q = order[(size_t)k];
       const int32_t c = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
       cnt[(size_t)(c - r0) + 1]++;
-      pairs[(size_t)q] = I2{c, (int32_t)k};  // slot k: contiguous per owner
+      targets[(size_t)q] = c;
+      slots[(size_t)q] = (int32_t)k;  // slot k: contiguous per owner
       wr[(size_t)t].push_back(spill_writer[(size_t)q]);
     }
     for (int32_t i = 0; i < T; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
     for (int32_t i = 0; i <= T; ++i) ip[i] = cnt[(size_t)i];
+    if (cnt[(size_t)T] >= 65536) bad = 2;
     auto& v = wr[(size_t)t];
     std::sort(v.begin(), v.end());
     v.erase(std::unique(v.begin(), v.end()), v.end());
@@ -213,6 +218,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
       writers.push_back(w);
     }
   }
+  if (bad == 2) return set_error(SYMM_ERR_UNSUPPORTED, "a tile receives >= 65536 staged contributions");
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "a writer tile does not precede its owner");
   { std::vector<std::vector<int32_t>>().swap(wr); }
   // tile blocks
@@ -227,8 +233,12 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
     uint16_t* tidx = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
+    uint16_t* inp = reinterpret_cast<uint16_t*>(blk + D.o_inptr);
+    int32_t* slt = reinterpret_cast<int32_t*>(blk + D.o_slot);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
     const int32_t e0 = S.prow_ptr[(size_t)r0];
+    for (int32_t i = 0; i <= T; ++i) inp[i] = (uint16_t)in_ptr[(size_t)(r0 + t + i)];
+    for (int32_t j = 0; j < ns; ++j) slt[j] = slots[(size_t)(S.spill_ptr[(size_t)t] + j)];
     std::vector<int32_t> tcnt((size_t)W + 1, 0);
     for (int32_t r = r0; r < r1; ++r) {
       start[r - r0] = (uint16_t)(S.prow_ptr[(size_t)r] - e0);
@@ -261,14 +271,14 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   TileDesc* d_desc;
   unsigned char* d_blocks;
-  I2* d_pairs;
-  int32_t *d_inptr, *d_writers;
+  int32_t* d_targets;
+  int32_t* d_writers;
   double* d_spill;
   unsigned long long* d_counter;
   unsigned int* d_ready;
   int rc;
   if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
-      (rc = upload(P, &d_pairs, pairs.data(), pairs.size())) || (rc = upload(P, &d_inptr, in_ptr.data(), in_ptr.size())) ||
+      (rc = upload(P, &d_targets, targets.data(), targets.size())) ||
       (rc = upload(P, &d_writers, writers.data(), writers.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)) ||
       (rc = dev_alloc(P, &d_counter, 1)) || (rc = dev_alloc(P, &d_ready, (size_t)std::max(nt, 1))))
     return rc;
@@ -278,8 +288,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   A.tiles = d_desc;
   A.ntiles = nt;
   A.blocks = d_blocks;
-  A.pairs = d_pairs;
-  A.in_ptr = d_inptr;
+  A.targets = d_targets;
   A.writers = d_writers;
   A.spill_buf = d_spill;
   A.ready = d_ready;
@@ -387,16 +396,16 @@ void race_config_default(race_config* c) {
   std::memset(c, 0, sizeof *c);
   c->k = 2;
   c->n_workers = 0;
-  c->tile_work = 4608;
+  c->tile_work = 2304;
   c->balance_by = 1;
   c->root = -1;
   c->n_eps = 3;
   c->eps[0] = 0.8;  // eps_0 = eps_1 = 0.8, eps_{s>1} = 0.5
   c->eps[1] = 0.8;
   for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
-  c->max_tile_rows = 2048;
-  c->max_tile_window = 2048;
-  c->max_tile_nnz = 4096;
+  c->max_tile_rows = 1024;
+  c->max_tile_window = 1024;
+  c->max_tile_nnz = 2048;
   c->reorder = 1;
   c->validate = 1;
   c->flags = 0;

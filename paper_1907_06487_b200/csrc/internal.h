@@ -63,19 +63,18 @@ void alg4_balance(std::vector<int32_t>& T_ptr, const std::vector<int32_t>& worke
 int build_schedule(const symm_csr_upper* U, const race_config* cfg, Schedule* S);
 
 // ---- device side -----------------------------------------------------------
-struct alignas(8) I2 {
-  int32_t x, y;
-};
-
 constexpr uint32_t kFirstBit = 0x80000000u;
 constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the persistent owner-computes kernel (K3).  64 bytes.
-// The tile's block (bulk-copied to shared memory) holds, 16-B aligned:
-//   start u16[T+1] | lcol u16[nnz] | tidx u16[noff] | tptr u16[W+1] | val f64[nnz]
+// The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
+//   start u16[T+1] | lcol u16[nnz] | tidx u16[noff] | tptr u16[W+1] |
+//   inptr u16[T+1] | slot i32[S] | val f64[nnz]
 // start: entry offsets of the T own rows (natural row order); lcol: local
 // column (own rows 0..T-1, then spill targets T..W-1); tidx/tptr: the
-// off-diagonal entries grouped by local target (CSC of the tile).
+// off-diagonal entries grouped by local target (CSC of the tile); inptr:
+// incoming staged contributions per own row; slot: where each spill target's
+// contribution is staged for its owner.
 struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
@@ -83,12 +82,11 @@ struct TileDesc {
   int32_t nspill;       // S (window W = T + S)
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
-  int32_t spill_off;    // first (target, slot) pair of this tile
-  int32_t in_off;       // first of the T+1 incoming pointers of this tile
+  int32_t spill_off;    // first spill target of this tile in `targets`
   int32_t in_base;      // first incoming slot in spill_buf
   int32_t nwr;          // writer tiles this tile waits for
   int32_t wr_off;       // first writer id
-  uint16_t o_lcol, o_tidx, o_tptr, o_val;  // byte offsets inside the block
+  uint16_t o_lcol, o_tidx, o_tptr, o_inptr, o_slot, o_val;  // byte offsets in the block
   int32_t pad;
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
@@ -97,8 +95,7 @@ struct TiledArgs {
   const TileDesc* tiles;          // tile id order (= BFS order = claim order)
   int32_t ntiles;
   const unsigned char* blocks;
-  const I2* pairs;                // per spill entry: (global target, incoming slot)
-  const int32_t* in_ptr;          // per tile T+1 incoming offsets (relative to in_base)
+  const int32_t* targets;         // per spill entry: global target row
   const int32_t* writers;         // writer tile ids per tile
   double* spill_buf;              // staged contributions to other tiles' rows
   unsigned int* ready;            // per tile: epoch when its spill contributions are staged

@@ -143,29 +143,33 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 }
 
 // ---------------------------------------------------------------- K3 tiled (owner computes)
-// Per tile (one CTA at a time, persistent grid, tiles claimed in BFS order):
-//   1. the whole tile block (matrix entries + CSC of the tile) arrives by one
-//      cp.async.bulk (TMA) into a double-buffered smem slot; the NEXT tile's
-//      block is already in flight while this one is computed;
-//   2. x of the tile window (own rows + spill targets) is gathered to smem;
-//   3. pass 1 (rows):    ys[i] = sum_e a_e x[c_e]          (tmp)
-//                        P[e]  = a_e x[i] for off-diagonal e
-//      pass 2 (targets): ys[l] += sum_{e: c_e = l} P[e]  (b[col] += ...)
-//      both passes are conflict-free and in a fixed order -> deterministic;
-//   4. contributions to rows of later tiles (spill) are staged in spill_buf,
-//      then the tile publishes `ready`;
-//   5. the owner of a row waits only for the tiles that wrote into its rows
-//      (all earlier in claim order, none of them waits before publishing:
-//      dependency depth 1, RACE's "local synchronisation"),
-//      adds their staged contributions in slot order and stores y once.
-// y is written exactly once per row: no pre-zeroing, no atomics.
-constexpr int kTiledThreads = 512;
+// Warp-specialised persistent kernel, tiles claimed in BFS order:
+//   producer warp: claims a tile, TMA-bulk-copies its block (matrix entries +
+//     CSC of the tile + staging slots) and cp.async-gathers x of the tile
+//     window (own rows + spill targets) into a 2-stage smem ring
+//     (mbarrier full/empty per stage);
+//   16 consumer warps:
+//     pass 1 (rows):    ys[i] = sum_e a_e x[c_e]            (tmp)
+//                       P[e]  = a_e x[i] for off-diagonal e
+//     pass 2 (targets): ys[l] += sum_{e: c_e = l} P[e]    (b[col] += ...)
+//     -> conflict-free, fixed order, deterministic; then contributions to
+//     rows of later tiles are staged in spill_buf, the tile waits only for the
+//     earlier tiles that wrote into its own rows (depth-1 dependencies: RACE's
+//     local synchronisation), adds their staged values in
+//     slot order and stores y once.  No pre-zeroing, no atomics on y.
+constexpr int kStages = 2;
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kTiledThreads = kConsumers + 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -185,69 +189,94 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__device__ __forceinline__ void issue_tile(const TiledArgs& A, long long t, unsigned char* buf, uint64_t* bar) {
-  const TileDesc& D = A.tiles[t];
-  fence_proxy_async();
-  mbar_arrive_expect_tx(bar, (unsigned)D.block_bytes);
-  bulk_g2s(buf, A.blocks + D.block_off, (unsigned)D.block_bytes, bar);
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
 template <int V>
 __global__ void __launch_bounds__(kTiledThreads) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                          double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ long long s_next;
-  unsigned char* buf0 = sm;
-  unsigned char* buf1 = sm + A.block_cap;
-  double* xs = reinterpret_cast<double*>(sm + 2 * (size_t)A.block_cap);
-  double* ys = xs + A.window_cap;
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ long long slot_tile[kStages];
+  const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
+  double* ys = reinterpret_cast<double*>(sm + kStages * slot_bytes);
   double* Pp = ys + A.window_cap;
-  constexpr int RPW = 32 / V;
-  constexpr int NW = kTiledThreads / 32;
-  const int tid = threadIdx.x, lane = tid & 31, sub = lane % V, wid = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 33);  // 32 producer lanes (cp.async noinc) + 1 expect_tx arrive
+      mbar_init(&empty[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    long long t = (long long)(atomicAdd(A.counter, 1ull) - A.claim_base);
-    s_next = t;
-    if (t < A.ntiles) issue_tile(A, t, buf0, &mbar[0]);
   }
   __syncthreads();
-  long long cur = s_next;
-  int b = 0;
-  unsigned par0 = 0, par1 = 0;
-  while (cur < A.ntiles) {
-    __syncthreads();  // every thread has read s_next
-    if (tid == 0) {
-      long long t = (long long)(atomicAdd(A.counter, 1ull) - A.claim_base);
-      s_next = t;
-      if (t < A.ntiles) issue_tile(A, t, b ? buf0 : buf1, b ? &mbar[0] : &mbar[1]);
+  if (wid == kConsumerWarps) {
+    // ------------------------------------------------ producer warp
+    for (int k = 0;; ++k) {
+      const int s = k % kStages;
+      const int use = k / kStages;
+      if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
+      long long t = 0;
+      if (lane == 0) t = (long long)(atomicAdd(A.counter, 1ull) - A.claim_base);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      unsigned char* blk = sm + s * slot_bytes;
+      double* xsl = reinterpret_cast<double*>(blk + A.block_cap);
+      if (t >= A.ntiles) {
+        if (lane == 0) {
+          slot_tile[s] = t;
+          mbar_arrive(&full[s]);
+        }
+        cp_async_arrive_noinc(&full[s]);
+        break;
+      }
+      const TileDesc& D = A.tiles[t];
+      if (lane == 0) {
+        slot_tile[s] = t;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&full[s], (unsigned)D.block_bytes);
+        bulk_g2s(blk, A.blocks + D.block_off, (unsigned)D.block_bytes, &full[s]);
+      }
+      const int T = D.nrows, S = D.nspill;
+      const double* xo = x + D.row0;
+      for (int i = lane; i < T; i += 32) cp_async8(xsl + i, xo + i);
+      const int32_t* tg = A.targets + D.spill_off;
+      for (int i = lane; i < S; i += 32) cp_async8(xsl + T + i, x + tg[i]);
+      cp_async_arrive_noinc(&full[s]);
     }
-    const TileDesc D = A.tiles[cur];
+    return;
+  }
+  // -------------------------------------------------- consumer warps
+  constexpr int RPW = 32 / V;
+  const int sub = lane % V;
+  for (int k = 0;; ++k) {
+    const int s = k % kStages;
+    mbar_wait(&full[s], (unsigned)((k / kStages) & 1));
+    const long long t = slot_tile[s];
+    if (t >= A.ntiles) break;
+    const TileDesc D = A.tiles[t];
     const int T = D.nrows, S = D.nspill, W = T + S;
-    const I2* pairs = A.pairs + D.spill_off;
-    for (int i = tid; i < T; i += kTiledThreads) xs[i] = x[D.row0 + i];
-    for (int i = tid; i < S; i += kTiledThreads) xs[T + i] = __ldg(x + pairs[i].x);
-    unsigned char* blk = b ? buf1 : buf0;
-    if (b) { mbar_wait(&mbar[1], par1); par1 ^= 1u; }
-    else { mbar_wait(&mbar[0], par0); par0 ^= 1u; }
-    __syncthreads();
+    const unsigned char* blk = sm + s * slot_bytes;
+    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk);
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
     const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
+    const uint16_t* inptr = reinterpret_cast<const uint16_t*>(blk + D.o_inptr);
+    const int32_t* slot = reinterpret_cast<const int32_t*>(blk + D.o_slot);
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    // pass 1: rows (V lanes per row)
-    for (int base = wid * RPW; base < T; base += NW * RPW) {
+    // pass 1: rows, V lanes per row
+    for (int base = wid * RPW; base < T; base += kConsumerWarps * RPW) {
       const int i = base + lane / V;
       double sum = 0.0;
       if (i < T) {
         const int eb = start[i], ee = start[i + 1];
         const double xi = xs[i];
+#pragma unroll 4
         for (int e = eb + sub; e < ee; e += V) {
           const int c = lcol[e];
           const double a = val[e];
@@ -258,38 +287,38 @@ __global__ void __launch_bounds__(kTiledThreads) k_tiled(TiledArgs A, const doub
       sum = group_sum<V>(sum);
       if (i < T && sub == 0) ys[i] = sum;
     }
-    __syncthreads();
+    consumer_sync();
     // pass 2: targets (one thread per local target, entries in stored order)
-    for (int l = tid; l < W; l += kTiledThreads) {
+    for (int l = tid; l < W; l += kConsumers) {
       double acc = l < T ? ys[l] : 0.0;
       const int jb = tptr[l], je = tptr[l + 1];
+#pragma unroll 4
       for (int j = jb; j < je; ++j) acc += Pp[tidx[j]];
       ys[l] = acc;
     }
-    __syncthreads();
-    // stage contributions to later tiles' rows, then publish
-    for (int i = tid; i < S; i += kTiledThreads) __stcg(A.spill_buf + pairs[i].y, ys[T + i]);
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) st_release_u32(A.ready + cur, A.epoch);
-    // wait for the writers of this tile's rows (all claimed earlier)
-    for (int k = tid; k < D.nwr; k += kTiledThreads) {
-      const unsigned int* f = A.ready + A.writers[D.wr_off + k];
-      while (ld_acquire_u32(f) != A.epoch) __nanosleep(32);
+    consumer_sync();
+    // stage contributions to later tiles' rows, then publish (before waiting:
+    // publication never depends on another tile -> dependency depth 1)
+    for (int i = tid; i < S; i += kConsumers) __stcg(A.spill_buf + slot[i], ys[T + i]);
+    if (S > 0) __threadfence();
+    consumer_sync();
+    if (tid == 0) st_release_u32(A.ready + t, A.epoch);
+    // wait for the (earlier) tiles that wrote into this tile's rows
+    for (int q = tid; q < D.nwr; q += kConsumers) {
+      const unsigned int* f = A.ready + A.writers[D.wr_off + q];
+      while (ld_acquire_u32(f) != A.epoch) __nanosleep(20);
       __threadfence();
     }
-    __syncthreads();
-    const int32_t* ip = A.in_ptr + D.in_off;
+    consumer_sync();
     const double* inb = A.spill_buf + D.in_base;
-    for (int i = tid; i < T; i += kTiledThreads) {
+    for (int i = tid; i < T; i += kConsumers) {
       double acc = ys[i];
-      const int jb = ip[i], je = ip[i + 1];
+      const int jb = inptr[i], je = inptr[i + 1];
       for (int j = jb; j < je; ++j) acc += __ldcg(inb + j);
       y[D.row0 + i] = acc;
     }
-    __syncthreads();
-    cur = s_next;
-    b ^= 1;
+    consumer_sync();  // slot s (block + x window) and ys/P are free again
+    if (tid == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -354,7 +383,7 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 }
 
 int tiled_smem_bytes(const TiledArgs& T) {
-  return 2 * T.block_cap + 2 * T.window_cap * 8 + T.nnz_cap * 8;
+  return kStages * (T.block_cap + 8 * T.window_cap) + 8 * T.window_cap + 8 * T.nnz_cap;
 }
 
 template <int V>
