@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="st27_128")
-    ap.add_argument("--variant", default="tiled", choices=["tiled", "atomic", "colored", "auto"])
+    ap.add_argument("--variant", default="tiled", choices=["tiled", "tiled_atomic", "atomic", "colored", "auto"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-variants", action="store_true", help="also time the other variants (extra key)")
@@ -280,7 +280,7 @@ def main():
 
     extra = {}
     if a.all_variants:
-        for v in ("atomic", "colored", "tiled"):
+        for v in ("atomic", "colored", "tiled", "tiled_atomic"):
             try:
                 m, l, _ = timed(v, max(50, a.steps // 4), 5)
                 extra[v] = {"ms_per_step": m, "gflops": 2.0 * nf / (m / 1e3) / 1e9,

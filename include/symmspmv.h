@@ -129,7 +129,8 @@ typedef enum {
   SYMM_VARIANT_AUTO = 0,    /* tiled if every tile fits, else colored                 */
   SYMM_VARIANT_COLORED = 1, /* K2: one launch per phase, global read-modify-write     */
   SYMM_VARIANT_ATOMIC = 2,  /* K1: one launch, native fp64 RED for transposed updates */
-  SYMM_VARIANT_TILED = 3    /* K3: persistent dataflow kernel, smem windows, ordered  */
+  SYMM_VARIANT_TILED = 3,   /* K3: TMA-staged tiles, smem two-pass, staged fixup; deterministic */
+  SYMM_VARIANT_TILED_ATOMIC = 4 /* K4: same tiles, window flushed with fp64 RED into zeroed y */
 } symm_variant;
 
 typedef enum { SYMM_ORDER_PERMUTED = 0, SYMM_ORDER_ORIGINAL = 1 } symm_vec_order;

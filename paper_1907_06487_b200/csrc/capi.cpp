@@ -57,6 +57,8 @@ struct symmspmv_plan {
   TiledArgs targs{};
   int tiled_grid = 0;
   int tiled_occ = 0;
+  int32_t* d_in_ptr = nullptr;
+  FixupArgs fargs{};
   // vector order / host staging
   int32_t *d_perm = nullptr, *d_inv = nullptr;
   double *d_xp = nullptr, *d_yp = nullptr;
@@ -115,7 +117,7 @@ int pick_vec(int64_t nnz, int32_t n) {
 
 static inline int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
 
-// K3 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order.
+// K3/K4 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order.
 int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   const int32_t nt = (int32_t)S.tile_group.size();
   const int32_t n = S.n;
@@ -124,10 +126,8 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     for (int32_t r = S.tile_ptr[(size_t)t]; r < S.tile_ptr[(size_t)t + 1]; ++r) tile_of[(size_t)r] = t;
   std::vector<TileDesc> desc((size_t)nt);
   std::vector<int64_t> boff((size_t)nt + 1, 0);
-  std::vector<int32_t> ndiag((size_t)nt, 0);
-  int32_t block_cap = 16, window_cap = 1, nnz_cap = 1;
+  int32_t block_cap = 16, window_cap = 2, nnz_cap = 2;
   int bad = 0;
-  // sizes
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
     const int32_t S_ = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
@@ -135,13 +135,12 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     int32_t nd = 0;
     for (int32_t r = r0; r < r1; ++r)
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
-    ndiag[(size_t)t] = nd;
     const int64_t W = (int64_t)T + S_;
     int64_t o_lcol = align16(2 * (int64_t)(T + 1));
     int64_t o_tidx = align16(o_lcol + 2 * nnz);
     int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
-    int64_t o_inptr = align16(o_tptr + 2 * (W + 1));
-    int64_t o_slot = align16(o_inptr + 2 * (int64_t)(T + 1));
+    int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
+    int64_t o_slot = align16(o_tgt + 4 * (int64_t)S_);
     int64_t o_val = align16(o_slot + 4 * (int64_t)S_);
     int64_t bytes = align16(o_val + 8 * nnz);
     if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
@@ -155,73 +154,29 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     D.o_lcol = (uint16_t)o_lcol;
     D.o_tidx = (uint16_t)o_tidx;
     D.o_tptr = (uint16_t)o_tptr;
-    D.o_inptr = (uint16_t)o_inptr;
+    D.o_tgt = (uint16_t)o_tgt;
     D.o_slot = (uint16_t)o_slot;
     D.o_val = (uint16_t)o_val;
     boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
     D.block_off = boff[(size_t)t];
-    D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
     block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
     window_cap = std::max<int32_t>(window_cap, (int32_t)W);
     nnz_cap = std::max<int32_t>(nnz_cap, (int32_t)nnz);
   }
   if (bad)
     return set_error(SYMM_ERR_UNSUPPORTED, "tile %d does not fit the 64 KB tile-block format (use smaller tiles)", bad - 1);
-  // incoming contributions: (owner tile, local target, writer, spill index) -> slot
+  window_cap = (window_cap + 15) & ~15;  // keeps every stage 128-B aligned
+  block_cap = (block_cap + 127) & ~127;
+  // staged contributions: slot order = (owner row, writer tile, ...) -> contiguous per row
   const int64_t nsp = (int64_t)S.spill.size();
-  std::vector<int32_t> targets((size_t)nsp), slots((size_t)nsp);
-  std::vector<int64_t> own_cnt((size_t)nt + 1, 0);
-  for (int64_t q = 0; q < nsp; ++q) own_cnt[(size_t)tile_of[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)] + 1]++;
-  for (int32_t t = 0; t < nt; ++t) own_cnt[(size_t)t + 1] += own_cnt[(size_t)t];
-  std::vector<int64_t> order((size_t)nsp);  // spill entry ids grouped by owner, writer-ascending
+  std::vector<int32_t> in_ptr((size_t)n + 1, 0), slots((size_t)nsp);
+  for (int64_t q = 0; q < nsp; ++q) in_ptr[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask) + 1]++;
+  for (int32_t r = 0; r < n; ++r) in_ptr[(size_t)r + 1] += in_ptr[(size_t)r];
   {
-    std::vector<int64_t> pos(own_cnt.begin(), own_cnt.end() - 1);
-    for (int64_t q = 0; q < nsp; ++q) order[(size_t)pos[(size_t)tile_of[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)]]++] = q;
+    std::vector<int32_t> pos(in_ptr.begin(), in_ptr.end() - 1);
+    for (int64_t q = 0; q < nsp; ++q)  // ascending writer tile, then ascending target
+      slots[(size_t)q] = pos[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)]++;
   }
-  std::vector<int32_t> in_ptr((size_t)n + (size_t)nt, 0);  // T+1 per tile at row0 + t
-  std::vector<std::vector<int32_t>> wr((size_t)nt);
-  std::vector<int32_t> spill_writer((size_t)nsp);
-  for (int32_t w = 0; w < nt; ++w)
-    for (int64_t q = S.spill_ptr[(size_t)w]; q < S.spill_ptr[(size_t)w + 1]; ++q) spill_writer[(size_t)q] = w;
-#pragma omp parallel for schedule(dynamic, 16)
-  for (int32_t t = 0; t < nt; ++t) {
-    const int32_t r0 = S.tile_ptr[(size_t)t], T = S.tile_ptr[(size_t)t + 1] - r0;
-    const int64_t b0 = own_cnt[(size_t)t], b1 = own_cnt[(size_t)t + 1];
-    // stable sort by target (writer order inside one target is preserved)
-    std::stable_sort(order.begin() + b0, order.begin() + b1, [&](int64_t a, int64_t b) {
-      return ((uint32_t)S.spill[(size_t)a] & kIdxMask) < ((uint32_t)S.spill[(size_t)b] & kIdxMask);
-    });
-    int32_t* ip = in_ptr.data() + r0 + t;
-    std::vector<int32_t> cnt((size_t)T + 1, 0);
-    for (int64_t k = b0; k < b1; ++k) {
-      const int64_t q = order[(size_t)k];
-      const int32_t c = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
-      cnt[(size_t)(c - r0) + 1]++;
-      targets[(size_t)q] = c;
-      slots[(size_t)q] = (int32_t)k;  // slot k: contiguous per owner
-      wr[(size_t)t].push_back(spill_writer[(size_t)q]);
-    }
-    for (int32_t i = 0; i < T; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
-    for (int32_t i = 0; i <= T; ++i) ip[i] = cnt[(size_t)i];
-    if (cnt[(size_t)T] >= 65536) bad = 2;
-    auto& v = wr[(size_t)t];
-    std::sort(v.begin(), v.end());
-    v.erase(std::unique(v.begin(), v.end()), v.end());
-    desc[(size_t)t].in_base = (int32_t)b0;
-  }
-  std::vector<int32_t> writers;
-  for (int32_t t = 0; t < nt; ++t) {
-    desc[(size_t)t].wr_off = (int32_t)writers.size();
-    desc[(size_t)t].nwr = (int32_t)wr[(size_t)t].size();
-    for (int32_t w : wr[(size_t)t]) {
-      if (w >= t) bad = 1;  // writers must precede owners in claim order
-      writers.push_back(w);
-    }
-  }
-  if (bad == 2) return set_error(SYMM_ERR_UNSUPPORTED, "a tile receives >= 65536 staged contributions");
-  if (bad) return set_error(SYMM_ERR_SCHEDULE, "a writer tile does not precede its owner");
-  { std::vector<std::vector<int32_t>>().swap(wr); }
-  // tile blocks
   std::vector<unsigned char> blocks((size_t)boff[(size_t)nt], 0);
 #pragma omp parallel for schedule(dynamic, 8) reduction(| : bad)
   for (int32_t t = 0; t < nt; ++t) {
@@ -233,12 +188,14 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
     uint16_t* tidx = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
-    uint16_t* inp = reinterpret_cast<uint16_t*>(blk + D.o_inptr);
+    int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
     int32_t* slt = reinterpret_cast<int32_t*>(blk + D.o_slot);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
+    for (int32_t j = 0; j < ns; ++j) {
+      tgt[j] = (int32_t)((uint32_t)sp[j] & kIdxMask);
+      slt[j] = slots[(size_t)(S.spill_ptr[(size_t)t] + j)];
+    }
     const int32_t e0 = S.prow_ptr[(size_t)r0];
-    for (int32_t i = 0; i <= T; ++i) inp[i] = (uint16_t)in_ptr[(size_t)(r0 + t + i)];
-    for (int32_t j = 0; j < ns; ++j) slt[j] = slots[(size_t)(S.spill_ptr[(size_t)t] + j)];
     std::vector<int32_t> tcnt((size_t)W + 1, 0);
     for (int32_t r = r0; r < r1; ++r) {
       start[r - r0] = (uint16_t)(S.prow_ptr[(size_t)r] - e0);
@@ -250,10 +207,10 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
           int32_t lo = 0, hi = ns;
           while (lo < hi) {
             int32_t mid = (lo + hi) / 2;
-            if ((int32_t)((uint32_t)sp[mid] & kIdxMask) < c) lo = mid + 1;
+            if (tgt[mid] < c) lo = mid + 1;
             else hi = mid;
           }
-          if (lo >= ns || (int32_t)((uint32_t)sp[lo] & kIdxMask) != c) bad |= 1;
+          if (lo >= ns || tgt[lo] != c) bad |= 1;
           l = T + lo;
         }
         lcol[i - e0] = (uint16_t)l;
@@ -271,35 +228,22 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   TileDesc* d_desc;
   unsigned char* d_blocks;
-  int32_t* d_targets;
-  int32_t* d_writers;
   double* d_spill;
-  unsigned long long* d_counter;
-  unsigned int* d_ready;
   int rc;
   if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
-      (rc = upload(P, &d_targets, targets.data(), targets.size())) ||
-      (rc = upload(P, &d_writers, writers.data(), writers.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)) ||
-      (rc = dev_alloc(P, &d_counter, 1)) || (rc = dev_alloc(P, &d_ready, (size_t)std::max(nt, 1))))
+      (rc = upload(P, &P->d_in_ptr, in_ptr.data(), in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)))
     return rc;
-  cudaMemset(d_counter, 0, sizeof(unsigned long long));
-  cudaMemset(d_ready, 0, sizeof(unsigned int) * (size_t)std::max(nt, 1));
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
   A.ntiles = nt;
   A.blocks = d_blocks;
-  A.targets = d_targets;
-  A.writers = d_writers;
   A.spill_buf = d_spill;
-  A.ready = d_ready;
-  A.epoch = 0;
-  A.counter = d_counter;
-  A.claim_base = 0;
   A.block_cap = block_cap;
   A.window_cap = window_cap;
   A.nnz_cap = nnz_cap;
+  P->fargs = FixupArgs{n, P->d_in_ptr, d_spill};
   if (tiled_smem_bytes(A) > 227 * 1024)
-    return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel needs %d B of shared memory", tiled_smem_bytes(A));
+    return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel needs %d B of shared memory (> 227 KB)", tiled_smem_bytes(A));
   int occ = 0;
   rc = tiled_max_ctas_per_sm(P->vec, A, &occ);
   if (rc) return cuda_fail((cudaError_t)rc, "occupancy query (tiled)");
@@ -355,12 +299,14 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     }
   } else if (variant == SYMM_VARIANT_TILED) {
     if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED was not uploaded by this plan");
-    TiledArgs A = P->targs;
-    A.epoch = P->targs.epoch + 1;
-    if ((rc = launch_tiled(A, x, y, P->vec, P->tiled_grid, st))) return cuda_fail((cudaError_t)rc, "k_tiled");
-    P->targs.epoch = A.epoch;
-    P->targs.claim_base += (unsigned long long)A.ntiles + (unsigned long long)P->tiled_grid;
-    P->last_launches = 1;
+    if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, false, st))) return cuda_fail((cudaError_t)rc, "k_tiled");
+    if ((rc = launch_fixup(P->fargs, y, st))) return cuda_fail((cudaError_t)rc, "k_fixup");
+    P->last_launches = 2;
+  } else if (variant == SYMM_VARIANT_TILED_ATOMIC) {
+    if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED_ATOMIC was not uploaded by this plan");
+    if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, true, st))) return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
+    P->last_launches = 2;
   } else {
     return set_error(SYMM_ERR_ARG, "unknown variant %d", variant);
   }
@@ -531,7 +477,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   if (U && (U->n != S.n || U->nnz != S.nnz))
     return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
                      (long long)U->nnz, S.n, (long long)S.nnz);
-  if (opt.variant < 0 || opt.variant > 3) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
+  if (opt.variant < 0 || opt.variant > 4) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
   if (opt.nranks != 1 || opt.rank != 0)
     return set_error(SYMM_ERR_UNSUPPORTED, "multi-rank plans are driven from Python in this version (nranks=%d)",
                      opt.nranks);
@@ -561,7 +507,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   int rc = SYMM_OK;
   const bool all = opt.build_all != 0;
   const int v = opt.variant;
-  bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_AUTO;
+  bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_TILED_ATOMIC || v == SYMM_VARIANT_AUTO;
   bool want_col = all || v == SYMM_VARIANT_COLORED;
   bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
   if (want_tiled) {

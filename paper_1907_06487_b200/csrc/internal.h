@@ -66,15 +66,14 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfg, Schedule* S)
 constexpr uint32_t kFirstBit = 0x80000000u;
 constexpr uint32_t kIdxMask = 0x7fffffffu;
 
-// One tile of the persistent owner-computes kernel (K3).  64 bytes.
+// One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
 //   start u16[T+1] | lcol u16[nnz] | tidx u16[noff] | tptr u16[W+1] |
-//   inptr u16[T+1] | slot i32[S] | val f64[nnz]
+//   tgt i32[S] | slot i32[S] | val f64[nnz]
 // start: entry offsets of the T own rows (natural row order); lcol: local
 // column (own rows 0..T-1, then spill targets T..W-1); tidx/tptr: the
-// off-diagonal entries grouped by local target (CSC of the tile); inptr:
-// incoming staged contributions per own row; slot: where each spill target's
-// contribution is staged for its owner.
+// off-diagonal entries grouped by local target (CSC of the tile); tgt: global
+// row of each spill target; slot: where K3 stages that contribution.
 struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
@@ -82,27 +81,23 @@ struct TileDesc {
   int32_t nspill;       // S (window W = T + S)
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
-  int32_t spill_off;    // first spill target of this tile in `targets`
-  int32_t in_base;      // first incoming slot in spill_buf
-  int32_t nwr;          // writer tiles this tile waits for
-  int32_t wr_off;       // first writer id
-  uint16_t o_lcol, o_tidx, o_tptr, o_inptr, o_slot, o_val;  // byte offsets in the block
-  int32_t pad;
+  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block
+  int32_t pad[6];
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
 
 struct TiledArgs {
-  const TileDesc* tiles;          // tile id order (= BFS order = claim order)
+  const TileDesc* tiles;          // tile id order (= BFS order)
   int32_t ntiles;
   const unsigned char* blocks;
-  const int32_t* targets;         // per spill entry: global target row
-  const int32_t* writers;         // writer tile ids per tile
-  double* spill_buf;              // staged contributions to other tiles' rows
-  unsigned int* ready;            // per tile: epoch when its spill contributions are staged
-  unsigned int epoch;
-  unsigned long long* counter;    // claim counter (monotone across runs)
-  unsigned long long claim_base;
+  double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
+};
+
+struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions
+  int32_t n;
+  const int32_t* in_ptr;          // [n+1] slots of row r: in_ptr[r] .. in_ptr[r+1]
+  const double* spill_buf;
 };
 
 struct CsrArgs {
@@ -126,7 +121,8 @@ int launch_zero(double* y, int64_t n, void* stream);
 int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream);
 int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x, double* y, int vec,
                          void* stream);
-int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, void* stream);
+int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream);
+int launch_fixup(const FixupArgs& F, double* y, void* stream);
 int tiled_smem_bytes(const TiledArgs& T);
 int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);

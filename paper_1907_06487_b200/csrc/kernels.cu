@@ -142,25 +142,26 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
   }
 }
 
-// ---------------------------------------------------------------- K3 tiled (owner computes)
-// Warp-specialised persistent kernel, tiles claimed in BFS order:
-//   producer warp: claims a tile, TMA-bulk-copies its block (matrix entries +
-//     CSC of the tile + staging slots) and cp.async-gathers x of the tile
-//     window (own rows + spill targets) into a 2-stage smem ring
-//     (mbarrier full/empty per stage);
+// ---------------------------------------------------------------- K3/K4 tiled streaming kernel
+// Persistent, static tile assignment (tile = blockIdx.x + k * gridDim.x, tiles
+// in BFS order), three warp roles on a kStages-deep smem ring:
+//   loader warp:  one cp.async.bulk (TMA) per tile block -> blk_full[s]
+//                 (waits for the consumers to free the stage: empty[s]);
+//   gather warp:  when a block has landed, cp.async-gathers x of the tile
+//                 window (own rows + spill targets) -> x_full[s];
 //   16 consumer warps:
 //     pass 1 (rows):    ys[i] = sum_e a_e x[c_e]            (tmp)
 //                       P[e]  = a_e x[i] for off-diagonal e
 //     pass 2 (targets): ys[l] += sum_{e: c_e = l} P[e]    (b[col] += ...)
-//     -> conflict-free, fixed order, deterministic; then contributions to
-//     rows of later tiles are staged in spill_buf, the tile waits only for the
-//     earlier tiles that wrote into its own rows (depth-1 dependencies: RACE's
-//     local synchronisation), adds their staged values in
-//     slot order and stores y once.  No pre-zeroing, no atomics on y.
-constexpr int kStages = 2;
+//     both conflict-free and in a fixed order; then the window is flushed:
+//       K3 (deterministic): own rows -> y (store), spill -> spill_buf[slot]
+//                           (then k_fixup adds the staged values in slot order);
+//       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
+// No consumer ever waits on global memory or on another CTA.
+constexpr int kStages = 4;
 constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kTiledThreads = kConsumers + 32;
+constexpr int kTiledThreads = kConsumers + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -197,76 +198,78 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
-template <int V>
-__global__ void __launch_bounds__(kTiledThreads) k_tiled(TiledArgs A, const double* __restrict__ x,
-                                                         double* __restrict__ y) {
+template <int V, bool ATOMIC>
+__global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
+                                                            double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ long long slot_tile[kStages];
+  __shared__ __align__(8) uint64_t blk_full[kStages], x_full[kStages], empty[kStages];
+  __shared__ __align__(16) TileDesc sdesc[kStages];
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   double* ys = reinterpret_cast<double*>(sm + kStages * slot_bytes);
   double* Pp = ys + A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 33);  // 32 producer lanes (cp.async noinc) + 1 expect_tx arrive
+      mbar_init(&blk_full[s], 1);
+      mbar_init(&x_full[s], 32);
       mbar_init(&empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (wid == kConsumerWarps) {
-    // ------------------------------------------------ producer warp
-    for (int k = 0;; ++k) {
-      const int s = k % kStages;
-      const int use = k / kStages;
-      if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
-      long long t = 0;
-      if (lane == 0) t = (long long)(atomicAdd(A.counter, 1ull) - A.claim_base);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      unsigned char* blk = sm + s * slot_bytes;
-      double* xsl = reinterpret_cast<double*>(blk + A.block_cap);
-      if (t >= A.ntiles) {
-        if (lane == 0) {
-          slot_tile[s] = t;
-          mbar_arrive(&full[s]);
-        }
-        cp_async_arrive_noinc(&full[s]);
-        break;
-      }
-      const TileDesc& D = A.tiles[t];
-      if (lane == 0) {
-        slot_tile[s] = t;
+    // ------------------------------------------------ loader warp (TMA bulk)
+    if (lane == 0) {
+      int k = 0;
+      for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+        const int s = k % kStages, use = k / kStages;
+        if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
+        const TileDesc& D = A.tiles[t];
+        const int64_t off = D.block_off;
+        const unsigned bytes = (unsigned)D.block_bytes;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&full[s], (unsigned)D.block_bytes);
-        bulk_g2s(blk, A.blocks + D.block_off, (unsigned)D.block_bytes, &full[s]);
+        mbar_arrive_expect_tx(&blk_full[s], bytes + (unsigned)sizeof(TileDesc));
+        bulk_g2s(&sdesc[s], A.tiles + t, (unsigned)sizeof(TileDesc), &blk_full[s]);
+        bulk_g2s(sm + s * slot_bytes, A.blocks + off, bytes, &blk_full[s]);
       }
+    }
+    return;
+  }
+  if (wid == kConsumerWarps + 1) {
+    // ------------------------------------------------ gather warp (x window)
+    int k = 0;
+    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+      const int s = k % kStages;
+      mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));
+      const TileDesc& D = sdesc[s];
+      const unsigned char* blk = sm + s * slot_bytes;
+      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap);
+      const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
       const int T = D.nrows, S = D.nspill;
       const double* xo = x + D.row0;
-      for (int i = lane; i < T; i += 32) cp_async8(xsl + i, xo + i);
-      const int32_t* tg = A.targets + D.spill_off;
-      for (int i = lane; i < S; i += 32) cp_async8(xsl + T + i, x + tg[i]);
-      cp_async_arrive_noinc(&full[s]);
+      for (int i = lane; i < T; i += 32) cp_async8(xs + i, xo + i);
+      for (int i = lane; i < S; i += 32) cp_async8(xs + T + i, x + tgt[i]);
+      cp_async_arrive_noinc(&x_full[s]);
     }
     return;
   }
   // -------------------------------------------------- consumer warps
   constexpr int RPW = 32 / V;
   const int sub = lane % V;
-  for (int k = 0;; ++k) {
+  int k = 0;
+  for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
     const int s = k % kStages;
-    mbar_wait(&full[s], (unsigned)((k / kStages) & 1));
-    const long long t = slot_tile[s];
-    if (t >= A.ntiles) break;
-    const TileDesc D = A.tiles[t];
-    const int T = D.nrows, S = D.nspill, W = T + S;
+    mbar_wait(&x_full[s], (unsigned)((k / kStages) & 1));
+    const TileDesc& D = sdesc[s];
+    const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
     const unsigned char* blk = sm + s * slot_bytes;
     const double* xs = reinterpret_cast<const double*>(blk + A.block_cap);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk);
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
     const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
-    const uint16_t* inptr = reinterpret_cast<const uint16_t*>(blk + D.o_inptr);
+    const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = reinterpret_cast<const int32_t*>(blk + D.o_slot);
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // pass 1: rows, V lanes per row
@@ -288,37 +291,35 @@ __global__ void __launch_bounds__(kTiledThreads) k_tiled(TiledArgs A, const doub
       if (i < T && sub == 0) ys[i] = sum;
     }
     consumer_sync();
-    // pass 2: targets (one thread per local target, entries in stored order)
+    // pass 2: targets, one thread per local target, entries in stored order; flush
     for (int l = tid; l < W; l += kConsumers) {
       double acc = l < T ? ys[l] : 0.0;
       const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
       for (int j = jb; j < je; ++j) acc += Pp[tidx[j]];
-      ys[l] = acc;
+      if (ATOMIC) {
+        atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
+      } else if (l < T) {
+        y[row0 + l] = acc;
+      } else {
+        __stcg(A.spill_buf + slot[l - T], acc);
+      }
     }
-    consumer_sync();
-    // stage contributions to later tiles' rows, then publish (before waiting:
-    // publication never depends on another tile -> dependency depth 1)
-    for (int i = tid; i < S; i += kConsumers) __stcg(A.spill_buf + slot[i], ys[T + i]);
-    if (S > 0) __threadfence();
-    consumer_sync();
-    if (tid == 0) st_release_u32(A.ready + t, A.epoch);
-    // wait for the (earlier) tiles that wrote into this tile's rows
-    for (int q = tid; q < D.nwr; q += kConsumers) {
-      const unsigned int* f = A.ready + A.writers[D.wr_off + q];
-      while (ld_acquire_u32(f) != A.epoch) __nanosleep(20);
-      __threadfence();
-    }
-    consumer_sync();
-    const double* inb = A.spill_buf + D.in_base;
-    for (int i = tid; i < T; i += kConsumers) {
-      double acc = ys[i];
-      const int jb = inptr[i], je = inptr[i + 1];
-      for (int j = jb; j < je; ++j) acc += __ldcg(inb + j);
-      y[D.row0 + i] = acc;
-    }
-    consumer_sync();  // slot s (block + x window) and ys/P are free again
+    consumer_sync();  // stage s and ys/P are free again
     if (tid == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// K3 second kernel: y[r] += staged contributions of row r in slot order.
+__global__ void __launch_bounds__(256) k_fixup(FixupArgs F, double* __restrict__ y) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; r < F.n; r += stride) {
+    const int jb = F.in_ptr[r], je = F.in_ptr[r + 1];
+    if (jb == je) continue;
+    double acc = y[r];
+    for (int j = jb; j < je; ++j) acc += __ldcs(F.spill_buf + j);
+    y[r] = acc;
   }
 }
 
@@ -386,19 +387,20 @@ int tiled_smem_bytes(const TiledArgs& T) {
   return kStages * (T.block_cap + 8 * T.window_cap) + 8 * T.window_cap + 8 * T.nnz_cap;
 }
 
-template <int V>
+template <int V, bool AT>
 static int tiled_setup(int smem) {
-  return (int)cudaFuncSetAttribute(k_tiled<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return (int)cudaFuncSetAttribute(k_tiled<V, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out) {
   const int smem = tiled_smem_bytes(T);
   int rc = 0, occ = 0;
   switch (vec) {
-#define OCC(VV)                                                                                                \
-  case VV:                                                                                                     \
-    rc = tiled_setup<VV>(smem);                                                                                \
-    if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<VV>, kTiledThreads, smem); \
+#define OCC(VV)                                                                                                   \
+  case VV:                                                                                                        \
+    rc = tiled_setup<VV, false>(smem);                                                                            \
+    if (!rc) rc = tiled_setup<VV, true>(smem);                                                                    \
+    if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<VV, false>, kTiledThreads, smem); \
     break;
     OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
 #undef OCC
@@ -408,18 +410,26 @@ int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out) {
   return rc;
 }
 
-int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, void* stream) {
+int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream) {
   if (T.ntiles <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = tiled_smem_bytes(T);
+#define LT(VV)                                                                            \
+  case VV:                                                                                \
+    if (atomic_flush) k_tiled<VV, true><<<grid, kTiledThreads, smem, st>>>(T, x, y);      \
+    else k_tiled<VV, false><<<grid, kTiledThreads, smem, st>>>(T, x, y);                  \
+    break;
   switch (vec) {
-    case 1: k_tiled<1><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
-    case 2: k_tiled<2><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
-    case 4: k_tiled<4><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
-    case 8: k_tiled<8><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
-    case 16: k_tiled<16><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
-    default: k_tiled<32><<<grid, kTiledThreads, smem, st>>>(T, x, y); break;
+    LT(1) LT(2) LT(4) LT(8) LT(16) LT(32)
+    default: return (int)cudaErrorInvalidValue;
   }
+#undef LT
+  return (int)cudaGetLastError();
+}
+
+int launch_fixup(const FixupArgs& F, double* y, void* stream) {
+  if (F.n <= 0) return 0;
+  k_fixup<<<grid_for(F.n, 256), 256, 0, (cudaStream_t)stream>>>(F, y);
   return (int)cudaGetLastError();
 }
 

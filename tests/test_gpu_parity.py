@@ -15,7 +15,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
-VARIANTS = ("atomic", "colored", "tiled")
+VARIANTS = ("atomic", "colored", "tiled", "tiled_atomic")
 
 
 def _torch():
@@ -57,7 +57,7 @@ SMALL = ["lap2d_64", "st27_24", "fem_knn_30k", "spin_14", "lap3d_40"]
 def test_parity_small_configs(name, variant):
     U, x = gen.make_config(name)
     y_ref = oracle.symmspmv(U, x)
-    outs, plan, _ = run_gpu(U, x, variant, repeats=3 if variant != "atomic" else 1)
+    outs, plan, _ = run_gpu(U, x, variant, repeats=3 if "atomic" not in variant else 1)
     assert relinf(outs[0], y_ref) <= TOL
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])  # colored/tiled: bitwise deterministic
@@ -103,7 +103,7 @@ def test_many_tiles_small_windows(variant):
     outs, _, s = run_gpu(U, x, variant, sched_kw=dict(tile_work=200, max_tile_window=512), repeats=3)
     assert s.stats["n_tiles"] > 300
     assert relinf(outs[0], oracle.symmspmv(U, x)) <= TOL
-    if variant != "atomic":
+    if "atomic" not in variant:
         assert all(np.array_equal(o, outs[0]) for o in outs)
 
 
@@ -160,7 +160,7 @@ def test_parity_full_size(name):
     plan = P.Plan(s, U, variant="auto", build_all=True)
     xd = torch.from_numpy(x[inv].copy()).cuda()
     yd = torch.empty_like(xd)
-    for v in ("tiled", "atomic"):
+    for v in ("tiled", "tiled_atomic", "atomic"):
         yd.fill_(float("nan"))
         plan.run(xd, yd, variant=v)
         torch.cuda.synchronize()
