@@ -144,24 +144,25 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 
 // ---------------------------------------------------------------- K3/K4 tiled streaming kernel
 // Persistent, static tile assignment (tile = blockIdx.x + k * gridDim.x, tiles
-// in BFS order), three warp roles on a kStages-deep smem ring:
-//   loader warp:  one cp.async.bulk (TMA) per tile block -> blk_full[s]
-//                 (waits for the consumers to free the stage: empty[s]);
+// in BFS order), warp roles on a kStages-deep smem ring:
+//   loader warp:  one cp.async.bulk (TMA) per tile block + descriptor ->
+//                 blk_full[s] (after the stage was released: empty[s]);
 //   gather warp:  when a block has landed, cp.async-gathers x of the tile
 //                 window (own rows + spill targets) -> x_full[s];
-//   16 consumer warps:
-//     pass 1 (rows):    ys[i] = sum_e a_e x[c_e]            (tmp)
-//                       P[e]  = a_e x[i] for off-diagonal e
-//     pass 2 (targets): ys[l] += sum_{e: c_e = l} P[e]    (b[col] += ...)
-//     both conflict-free and in a fixed order; then the window is flushed:
+//   2 consumer groups x 8 warps, alternating tiles (their passes overlap):
+//     pass A (thread per own row i):  ys[i] = sum_e a_e x[c_e]   (tmp)
+//                                     P[e]  = a_e x[i]           (off-diagonal e)
+//     pass B (thread per target l):   ys[l] += sum_{e: c_e = l} P[e]
+//     both conflict-free, fixed order -> deterministic; pass B flushes:
 //       K3 (deterministic): own rows -> y (store), spill -> spill_buf[slot]
-//                           (then k_fixup adds the staged values in slot order);
+//                           (k_fixup then adds the staged values in slot order);
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
-constexpr int kStages = 4;
-constexpr int kConsumerWarps = 16;
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kTiledThreads = kConsumers + 64;
+constexpr int kStages = 3;
+constexpr int kGroupWarps = 8;
+constexpr int kGroupThreads = kGroupWarps * 32;
+constexpr int kGroups = 2;
+constexpr int kTiledThreads = kGroups * kGroupThreads + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -196,17 +197,17 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
+__device__ __forceinline__ void group_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
+}
 
-template <int V, bool ATOMIC>
+template <bool ATOMIC>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t blk_full[kStages], x_full[kStages], empty[kStages];
   __shared__ __align__(16) TileDesc sdesc[kStages];
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
-  double* ys = reinterpret_cast<double*>(sm + kStages * slot_bytes);
-  double* Pp = ys + A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
   if (tid == 0) {
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (wid == kConsumerWarps) {
+  if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
     if (lane == 0) {
       int k = 0;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     }
     return;
   }
-  if (wid == kConsumerWarps + 1) {
+  if (wid == kGroups * kGroupWarps + 1) {
     // ------------------------------------------------ gather warp (x window)
     int k = 0;
     for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
@@ -254,11 +255,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     }
     return;
   }
-  // -------------------------------------------------- consumer warps
-  constexpr int RPW = 32 / V;
-  const int sub = lane % V;
-  int k = 0;
-  for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+  // -------------------------------------------------- consumer groups
+  const int g = wid / kGroupWarps;
+  const int gt = tid - g * kGroupThreads;
+  double* ys = reinterpret_cast<double*>(sm + kStages * slot_bytes) + (size_t)g * (A.window_cap + A.nnz_cap);
+  double* Pp = ys + A.window_cap;
+  int k = g;
+  for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % kStages;
     mbar_wait(&x_full[s], (unsigned)((k / kStages) & 1));
     const TileDesc& D = sdesc[s];
@@ -272,27 +275,22 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = reinterpret_cast<const int32_t*>(blk + D.o_slot);
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    // pass 1: rows, V lanes per row
-    for (int base = wid * RPW; base < T; base += kConsumerWarps * RPW) {
-      const int i = base + lane / V;
+    // pass A: one thread per own row
+    for (int i = gt; i < T; i += kGroupThreads) {
+      const int eb = start[i], ee = start[i + 1];
+      const double xi = xs[i];
       double sum = 0.0;
-      if (i < T) {
-        const int eb = start[i], ee = start[i + 1];
-        const double xi = xs[i];
 #pragma unroll 4
-        for (int e = eb + sub; e < ee; e += V) {
-          const int c = lcol[e];
-          const double a = val[e];
-          sum += a * xs[c];
-          if (c != i) Pp[e] = a * xi;
-        }
+      for (int e = eb; e < ee; ++e) {
+        const double a = val[e];
+        sum += a * xs[lcol[e]];
+        Pp[e] = a * xi;  // the diagonal's P is never read (not in the CSC lists)
       }
-      sum = group_sum<V>(sum);
-      if (i < T && sub == 0) ys[i] = sum;
+      ys[i] = sum;
     }
-    consumer_sync();
-    // pass 2: targets, one thread per local target, entries in stored order; flush
-    for (int l = tid; l < W; l += kConsumers) {
+    group_sync(g);
+    // pass B: one thread per local target, CSC entries in stored order; flush
+    for (int l = gt; l < W; l += kGroupThreads) {
       double acc = l < T ? ys[l] : 0.0;
       const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
@@ -305,8 +303,8 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         __stcg(A.spill_buf + slot[l - T], acc);
       }
     }
-    consumer_sync();  // stage s and ys/P are free again
-    if (tid == 0) mbar_arrive(&empty[s]);
+    group_sync(g);  // stage s and this group's ys/P are free again
+    if (gt == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -384,46 +382,27 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 }
 
 int tiled_smem_bytes(const TiledArgs& T) {
-  return kStages * (T.block_cap + 8 * T.window_cap) + 8 * T.window_cap + 8 * T.nnz_cap;
-}
-
-template <int V, bool AT>
-static int tiled_setup(int smem) {
-  return (int)cudaFuncSetAttribute(k_tiled<V, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return kStages * (T.block_cap + 8 * T.window_cap) + kGroups * 8 * (T.window_cap + T.nnz_cap);
 }
 
 int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out) {
+  (void)vec;
   const int smem = tiled_smem_bytes(T);
-  int rc = 0, occ = 0;
-  switch (vec) {
-#define OCC(VV)                                                                                                   \
-  case VV:                                                                                                        \
-    rc = tiled_setup<VV, false>(smem);                                                                            \
-    if (!rc) rc = tiled_setup<VV, true>(smem);                                                                    \
-    if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<VV, false>, kTiledThreads, smem); \
-    break;
-    OCC(1) OCC(2) OCC(4) OCC(8) OCC(16) OCC(32)
-#undef OCC
-    default: rc = (int)cudaErrorInvalidValue;
-  }
+  int rc = (int)cudaFuncSetAttribute(k_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (!rc) rc = (int)cudaFuncSetAttribute(k_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int occ = 0;
+  if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<false>, kTiledThreads, smem);
   *out = occ;
   return rc;
 }
 
 int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream) {
+  (void)vec;
   if (T.ntiles <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = tiled_smem_bytes(T);
-#define LT(VV)                                                                            \
-  case VV:                                                                                \
-    if (atomic_flush) k_tiled<VV, true><<<grid, kTiledThreads, smem, st>>>(T, x, y);      \
-    else k_tiled<VV, false><<<grid, kTiledThreads, smem, st>>>(T, x, y);                  \
-    break;
-  switch (vec) {
-    LT(1) LT(2) LT(4) LT(8) LT(16) LT(32)
-    default: return (int)cudaErrorInvalidValue;
-  }
-#undef LT
+  if (atomic_flush) k_tiled<true><<<grid, kTiledThreads, smem, st>>>(T, x, y);
+  else k_tiled<false><<<grid, kTiledThreads, smem, st>>>(T, x, y);
   return (int)cudaGetLastError();
 }
 
