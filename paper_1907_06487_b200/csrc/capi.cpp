@@ -157,6 +157,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     D.o_tgt = (uint16_t)o_tgt;
     D.o_slot = (uint16_t)o_slot;
     D.o_val = (uint16_t)o_val;
+    D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
     boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
     D.block_off = boff[(size_t)t];
     block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
@@ -165,7 +166,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   }
   if (bad)
     return set_error(SYMM_ERR_UNSUPPORTED, "tile %d does not fit the 64 KB tile-block format (use smaller tiles)", bad - 1);
-  window_cap = (window_cap + 15) & ~15;  // keeps every stage 128-B aligned
+  window_cap = (window_cap + 2 + 15) & ~15;  // +2: x window alignment shift; stages stay 128-B aligned
   block_cap = (block_cap + 127) & ~127;
   // staged contributions: slot order = (owner row, writer tile, ...) -> contiguous per row
   const int64_t nsp = (int64_t)S.spill.size();
@@ -229,14 +230,19 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   TileDesc* d_desc;
   unsigned char* d_blocks;
   double* d_spill;
+  int32_t* d_targets;
+  std::vector<int32_t> targets((size_t)nsp);
+  for (int64_t q = 0; q < nsp; ++q) targets[(size_t)q] = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
   int rc;
   if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
+      (rc = upload(P, &d_targets, targets.data(), targets.size())) ||
       (rc = upload(P, &P->d_in_ptr, in_ptr.data(), in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)))
     return rc;
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
   A.ntiles = nt;
   A.blocks = d_blocks;
+  A.targets = d_targets;
   A.spill_buf = d_spill;
   A.block_cap = block_cap;
   A.window_cap = window_cap;
@@ -342,7 +348,7 @@ void race_config_default(race_config* c) {
   std::memset(c, 0, sizeof *c);
   c->k = 2;
   c->n_workers = 0;
-  c->tile_work = 2304;
+  c->tile_work = 1792;
   c->balance_by = 1;
   c->root = -1;
   c->n_eps = 3;
@@ -350,8 +356,8 @@ void race_config_default(race_config* c) {
   c->eps[1] = 0.8;
   for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
   c->max_tile_rows = 1024;
-  c->max_tile_window = 1024;
-  c->max_tile_nnz = 2048;
+  c->max_tile_window = 768;
+  c->max_tile_nnz = 1536;
   c->reorder = 1;
   c->validate = 1;
   c->flags = 0;

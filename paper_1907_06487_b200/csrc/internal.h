@@ -70,6 +70,7 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
 //   start u16[T+1] | lcol u16[nnz] | tidx u16[noff] | tptr u16[W+1] |
 //   tgt i32[S] | slot i32[S] | val f64[nnz]
+// (tgt is also kept in the global `targets` array for the x-gather warp)
 // start: entry offsets of the T own rows (natural row order); lcol: local
 // column (own rows 0..T-1, then spill targets T..W-1); tidx/tptr: the
 // off-diagonal entries grouped by local target (CSC of the tile); tgt: global
@@ -82,7 +83,8 @@ struct TileDesc {
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
   uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block
-  int32_t pad[6];
+  int32_t spill_off;    // first spill target of this tile in `targets`
+  int32_t pad[5];
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
 
@@ -90,6 +92,7 @@ struct TiledArgs {
   const TileDesc* tiles;          // tile id order (= BFS order)
   int32_t ntiles;
   const unsigned char* blocks;
+  const int32_t* targets;         // spill targets of all tiles (tile order)
   double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
 };

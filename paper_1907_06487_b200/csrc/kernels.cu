@@ -158,7 +158,8 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //                           (k_fixup then adds the staged values in slot order);
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
-constexpr int kStages = 3;
+constexpr int kStages = 5;
+constexpr int kGatherRegs = 24;  // spill targets per gather lane held in registers (W cap 768)
 constexpr int kGroupWarps = 8;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 2;
@@ -221,37 +222,73 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   __syncthreads();
   if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
+    // per tile: descriptor + block + the 16-B aligned part of x[row0 .. row0+T)
     if (lane == 0) {
       int k = 0;
-      for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+      int t = blockIdx.x;
+      int64_t off = 0;
+      unsigned bytes = 0;
+      int row0 = 0, T = 0;
+      if (t < A.ntiles) {
+        off = A.tiles[t].block_off; bytes = (unsigned)A.tiles[t].block_bytes;
+        row0 = A.tiles[t].row0; T = A.tiles[t].nrows;
+      }
+      for (; t < A.ntiles; t += G, ++k) {
         const int s = k % kStages, use = k / kStages;
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
-        const TileDesc& D = A.tiles[t];
-        const int64_t off = D.block_off;
-        const unsigned bytes = (unsigned)D.block_bytes;
+        const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);  // 1: x+row0 is 8 mod 16
+        const int nfull = T > p ? ((T - p) & ~1) : 0;           // aligned element pairs
+        const unsigned xbytes = (unsigned)nfull * 8u;
+        double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&blk_full[s], bytes + (unsigned)sizeof(TileDesc));
+        mbar_arrive_expect_tx(&blk_full[s], bytes + (unsigned)sizeof(TileDesc) + xbytes);
         bulk_g2s(&sdesc[s], A.tiles + t, (unsigned)sizeof(TileDesc), &blk_full[s]);
         bulk_g2s(sm + s * slot_bytes, A.blocks + off, bytes, &blk_full[s]);
+        if (xbytes) bulk_g2s(xs + p, x + row0 + p, xbytes, &blk_full[s]);
+        const int tn = t + G;  // prefetch the next descriptor
+        if (tn < A.ntiles) {
+          off = A.tiles[tn].block_off; bytes = (unsigned)A.tiles[tn].block_bytes;
+          row0 = A.tiles[tn].row0; T = A.tiles[tn].nrows;
+        }
       }
     }
     return;
   }
   if (wid == kGroups * kGroupWarps + 1) {
     // ------------------------------------------------ gather warp (x window)
+    // spill targets of the NEXT tile are prefetched into registers while the
+    // current tile's cp.async gathers are in flight.
+    constexpr int kTg = kGatherRegs;
     int k = 0;
-    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
-      const int s = k % kStages;
-      mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));
-      const TileDesc& D = sdesc[s];
-      const unsigned char* blk = sm + s * slot_bytes;
-      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap);
-      const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
-      const int T = D.nrows, S = D.nspill;
-      const double* xo = x + D.row0;
-      for (int i = lane; i < T; i += 32) cp_async8(xs + i, xo + i);
-      for (int i = lane; i < S; i += 32) cp_async8(xs + T + i, x + tgt[i]);
+    int t = blockIdx.x;
+    int row0 = 0, T = 0, S = 0, soff = 0;
+    int32_t tg[kTg];
+    auto fetch = [&](int tt) {
+      row0 = A.tiles[tt].row0; T = A.tiles[tt].nrows; S = A.tiles[tt].nspill; soff = A.tiles[tt].spill_off;
+#pragma unroll
+      for (int j = 0; j < kTg; ++j) {
+        const int idx = lane + 32 * j;
+        tg[j] = idx < S ? __ldg(A.targets + soff + idx) : 0;
+      }
+    };
+    if (t < A.ntiles) fetch(t);
+    for (; t < A.ntiles; t += G, ++k) {
+      const int s = k % kStages, use = k / kStages;
+      if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
+      const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
+      const int nfull = T > p ? ((T - p) & ~1) : 0;
+      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
+      // own elements outside the bulk-copied aligned range: [0, p) and [p + nfull, T)
+      if (lane == 0 && p == 1) cp_async8(xs, x + row0);
+      if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
+#pragma unroll
+      for (int j = 0; j < kTg; ++j) {
+        const int idx = lane + 32 * j;
+        if (idx < S) cp_async8(xs + T + idx, x + tg[j]);
+      }
+      for (int idx = 32 * kTg + lane; idx < S; idx += 32) cp_async8(xs + T + idx, x + __ldg(A.targets + soff + idx));
       cp_async_arrive_noinc(&x_full[s]);
+      if (t + G < A.ntiles) fetch(t + G);
     }
     return;
   }
@@ -263,11 +300,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % kStages;
+    mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));
     mbar_wait(&x_full[s], (unsigned)((k / kStages) & 1));
     const TileDesc& D = sdesc[s];
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
     const unsigned char* blk = sm + s * slot_bytes;
-    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap);
+    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk);
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
     const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
