@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
 constexpr int kStages = 5;
-constexpr int kGatherRegs = 24;  // spill targets per gather lane held in registers (W cap 768)
 constexpr int kGroupWarps = 8;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 2;
@@ -256,39 +255,26 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   }
   if (wid == kGroups * kGroupWarps + 1) {
     // ------------------------------------------------ gather warp (x window)
-    // spill targets of the NEXT tile are prefetched into registers while the
-    // current tile's cp.async gathers are in flight.
-    constexpr int kTg = kGatherRegs;
+    // waits for the tile block (the loader runs kStages tiles ahead, so it has
+    // usually landed), reads the spill targets from shared memory and issues
+    // the x gathers: no global-latency chain per tile.
     int k = 0;
-    int t = blockIdx.x;
-    int row0 = 0, T = 0, S = 0, soff = 0;
-    int32_t tg[kTg];
-    auto fetch = [&](int tt) {
-      row0 = A.tiles[tt].row0; T = A.tiles[tt].nrows; S = A.tiles[tt].nspill; soff = A.tiles[tt].spill_off;
-#pragma unroll
-      for (int j = 0; j < kTg; ++j) {
-        const int idx = lane + 32 * j;
-        tg[j] = idx < S ? __ldg(A.targets + soff + idx) : 0;
-      }
-    };
-    if (t < A.ntiles) fetch(t);
-    for (; t < A.ntiles; t += G, ++k) {
-      const int s = k % kStages, use = k / kStages;
-      if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
+    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+      const int s = k % kStages;
+      mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));
+      const TileDesc& D = sdesc[s];
+      const int row0 = D.row0, T = D.nrows, S = D.nspill;
+      const unsigned char* blk = sm + s * slot_bytes;
+      const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
       const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
       const int nfull = T > p ? ((T - p) & ~1) : 0;
       double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
       // own elements outside the bulk-copied aligned range: [0, p) and [p + nfull, T)
       if (lane == 0 && p == 1) cp_async8(xs, x + row0);
       if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
-#pragma unroll
-      for (int j = 0; j < kTg; ++j) {
-        const int idx = lane + 32 * j;
-        if (idx < S) cp_async8(xs + T + idx, x + tg[j]);
-      }
-      for (int idx = 32 * kTg + lane; idx < S; idx += 32) cp_async8(xs + T + idx, x + __ldg(A.targets + soff + idx));
+#pragma unroll 4
+      for (int idx = lane; idx < S; idx += 32) cp_async8(xs + T + idx, x + tgt[idx]);
       cp_async_arrive_noinc(&x_full[s]);
-      if (t + G < A.ntiles) fetch(t + G);
     }
     return;
   }
@@ -300,7 +286,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % kStages;
-    mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));
+    mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));  // TMA data visible to this thread
     mbar_wait(&x_full[s], (unsigned)((k / kStages) & 1));
     const TileDesc& D = sdesc[s];
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
