@@ -137,7 +137,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
     const int64_t W = (int64_t)T + S_;
     int64_t o_lcol = align16(2 * (int64_t)(T + 1));
-    int64_t o_tidx = align16(o_lcol + 2 * nnz);
+    int64_t o_tidx = align16(o_lcol + 4 * nnz);
     int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
     int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
     int64_t o_slot = align16(o_tgt + 4 * (int64_t)S_);
@@ -186,7 +186,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
     unsigned char* blk = blocks.data() + D.block_off;
     uint16_t* start = reinterpret_cast<uint16_t*>(blk);
-    uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
+    uint32_t* rcol = reinterpret_cast<uint32_t*>(blk + D.o_lcol);
     uint16_t* tidx = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
@@ -214,7 +214,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
           if (lo >= ns || tgt[lo] != c) bad |= 1;
           l = T + lo;
         }
-        lcol[i - e0] = (uint16_t)l;
+        rcol[i - e0] = ((uint32_t)(r - r0) << 16) | (uint32_t)l;
         val[i - e0] = S.pval[(size_t)i];
         if (c != r) tcnt[(size_t)l + 1]++;
       }
@@ -224,7 +224,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     for (int32_t l = 0; l <= W; ++l) tptr[l] = (uint16_t)tcnt[(size_t)l];
     for (int32_t r = r0; r < r1; ++r)
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
-        if (S.pcol[(size_t)i] != r) tidx[tcnt[lcol[i - e0]]++] = (uint16_t)(i - e0);
+        if (S.pcol[(size_t)i] != r) tidx[tcnt[rcol[i - e0] & 0xffffu]++] = (uint16_t)(i - e0);
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   TileDesc* d_desc;

@@ -68,11 +68,12 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
-//   start u16[T+1] | lcol u16[nnz] | tidx u16[noff] | tptr u16[W+1] |
+//   start u16[T+1] | rc u32[nnz] | tidx u16[noff] | tptr u16[W+1] |
 //   tgt i32[S] | slot i32[S] | val f64[nnz]
+// rc[e] = (local row << 16) | local column of entry e
 // (tgt is also kept in the global `targets` array for the x-gather warp)
-// start: entry offsets of the T own rows (natural row order); lcol: local
-// column (own rows 0..T-1, then spill targets T..W-1); tidx/tptr: the
+// start: entry offsets of the T own rows (natural row order); local columns:
+// own rows 0..T-1, then spill targets T..W-1; tidx/tptr: the
 // off-diagonal entries grouped by local target (CSC of the tile); tgt: global
 // row of each spill target; slot: where K3 stages that contribution.
 struct TileDesc {

@@ -150,15 +150,15 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //   gather warp:  when a block has landed, cp.async-gathers x of the tile
 //                 window (own rows + spill targets) -> x_full[s];
 //   2 consumer groups x 8 warps, alternating tiles (their passes overlap):
-//     pass A (thread per own row i):  ys[i] = sum_e a_e x[c_e]   (tmp)
-//                                     P[e]  = a_e x[i]           (off-diagonal e)
-//     pass B (thread per target l):   ys[l] += sum_{e: c_e = l} P[e]
+//     pass A (entry-parallel):        PQ[e] = (a_e x[r_e], a_e x[c_e])
+//     pass B (thread per target l):   y_l = sum_{e in row l} Q[e]            (tmp)
+//                                         + sum_{e: c_e = l, e off-diag} P[e]
 //     both conflict-free, fixed order -> deterministic; pass B flushes:
 //       K3 (deterministic): own rows -> y (store), spill -> spill_buf[slot]
 //                           (k_fixup then adds the staged values in slot order);
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
-constexpr int kStages = 5;
+constexpr int kStages = 4;
 constexpr int kGroupWarps = 8;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 2;
@@ -281,8 +281,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // -------------------------------------------------- consumer groups
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
-  double* ys = reinterpret_cast<double*>(sm + kStages * slot_bytes) + (size_t)g * (A.window_cap + A.nnz_cap);
-  double* Pp = ys + A.window_cap;
+  double2* PQ = reinterpret_cast<double2*>(sm + kStages * slot_bytes) + (size_t)g * A.nnz_cap;
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % kStages;
@@ -293,32 +292,32 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const unsigned char* blk = sm + s * slot_bytes;
     const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk);
-    const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
+    const uint32_t* rcol = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
     const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = reinterpret_cast<const int32_t*>(blk + D.o_slot);
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    // pass A: one thread per own row
-    for (int i = gt; i < T; i += kGroupThreads) {
-      const int eb = start[i], ee = start[i + 1];
-      const double xi = xs[i];
-      double sum = 0.0;
-#pragma unroll 4
-      for (int e = eb; e < ee; ++e) {
-        const double a = val[e];
-        sum += a * xs[lcol[e]];
-        Pp[e] = a * xi;  // the diagonal's P is never read (not in the CSC lists)
-      }
-      ys[i] = sum;
+    const int nnz = D.nnz;
+    // pass A: entry-parallel products  PQ[e] = (a_e x[row_e], a_e x[col_e])
+    for (int e = gt; e < nnz; e += kGroupThreads) {
+      const uint32_t rc = rcol[e];
+      const double a = val[e];
+      PQ[e] = make_double2(a * xs[rc >> 16], a * xs[rc & 0xffffu]);
     }
     group_sync(g);
-    // pass B: one thread per local target, CSC entries in stored order; flush
+    // pass B: one thread per local target: own row sum (tmp)
+    // + transposed contributions, fixed order; then the flush
     for (int l = gt; l < W; l += kGroupThreads) {
-      double acc = l < T ? ys[l] : 0.0;
+      double acc = 0.0;
+      if (l < T) {
+        const int eb = start[l], ee = start[l + 1];
+#pragma unroll 4
+        for (int e = eb; e < ee; ++e) acc += PQ[e].y;
+      }
       const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
-      for (int j = jb; j < je; ++j) acc += Pp[tidx[j]];
+      for (int j = jb; j < je; ++j) acc += PQ[tidx[j]].x;
       if (ATOMIC) {
         atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
       } else if (l < T) {
@@ -327,7 +326,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         __stcg(A.spill_buf + slot[l - T], acc);
       }
     }
-    group_sync(g);  // stage s and this group's ys/P are free again
+    group_sync(g);  // stage s and this group's PQ are free again
     if (gt == 0) mbar_arrive(&empty[s]);
   }
 }
@@ -406,7 +405,7 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 }
 
 int tiled_smem_bytes(const TiledArgs& T) {
-  return kStages * (T.block_cap + 8 * T.window_cap) + kGroups * 8 * (T.window_cap + T.nnz_cap);
+  return kStages * (T.block_cap + 8 * T.window_cap) + kGroups * 16 * T.nnz_cap;
 }
 
 int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out) {
