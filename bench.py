@@ -331,7 +331,8 @@ def main():
         "schedule": {"build_s": t_sched, "plan_s": t_plan, "gen_s": t_gen, "tiles": st["n_tiles"],
                      "phases": st["n_phases"], "levels": st["total_levels"], "eta": st["eta"],
                      "max_subcolors": st["max_subcolors"], "mean_subcolors": st["mean_subcolors"],
-                     "bw_before": st["bandwidth_before"], "bw_after": st["bandwidth_after"]},
+                     "bw_before": st["bandwidth_before"], "bw_after": st["bandwidth_after"],
+                     "spill_entries": st["spill_entries"], "device_bytes": dev_bytes},
     }
     if extra:
         line["variants"] = extra

@@ -348,7 +348,7 @@ void race_config_default(race_config* c) {
   std::memset(c, 0, sizeof *c);
   c->k = 2;
   c->n_workers = 0;
-  c->tile_work = 1792;
+  c->tile_work = 1280;
   c->balance_by = 1;
   c->root = -1;
   c->n_eps = 3;
@@ -357,7 +357,7 @@ void race_config_default(race_config* c) {
   for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
   c->max_tile_rows = 1024;
   c->max_tile_window = 768;
-  c->max_tile_nnz = 1536;
+  c->max_tile_nnz = 1024;
   c->reorder = 1;
   c->validate = 1;
   c->flags = 0;

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //                           (k_fixup then adds the staged values in slot order);
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
-constexpr int kStages = 4;
+constexpr int kStages = 8;
 constexpr int kGroupWarps = 8;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 2;
