@@ -332,7 +332,7 @@ def main():
                      "phases": st["n_phases"], "levels": st["total_levels"], "eta": st["eta"],
                      "max_subcolors": st["max_subcolors"], "mean_subcolors": st["mean_subcolors"],
                      "bw_before": st["bandwidth_before"], "bw_after": st["bandwidth_after"],
-                     "spill_entries": st["spill_entries"], "device_bytes": dev_bytes},
+                     "spill_entries": st["spill_entries"], "device_bytes": dev_bytes, "plan": plan.info()},
     }
     if extra:
         line["variants"] = extra

@@ -178,6 +178,11 @@ int symmspmv_last_launches(const symmspmv_plan_t* p);
  * the chosen variant (12 nnz + 4 (n+1) + 24 n). */
 int symmspmv_plan_bytes(const symmspmv_plan_t* p, int64_t* device_bytes, int64_t* min_bytes);
 
+/* Launch configuration of the plan (diagnostics): out[0..7] = default variant,
+ * lanes per row, tiled grid, tiled smem ring depth, tile block cap (B),
+ * tile window cap, tile nnz cap, tiled dynamic smem (B).  Returns the count. */
+int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n);
+
 int symmspmv_destroy(symmspmv_plan_t* p);
 
 const char* symm_status_string(int status);

@@ -178,6 +178,12 @@ class Plan:
     def last_launches(self) -> int:
         return int(lib().symmspmv_last_launches(self._h))
 
+    def info(self) -> dict:
+        out = (C.c_int32 * 8)()
+        m = lib().symmspmv_plan_info(self._h, out, 8)
+        keys = ["variant", "vec", "tiled_grid", "tiled_stages", "block_cap", "window_cap", "nnz_cap", "tiled_smem"]
+        return {keys[i]: int(out[i]) for i in range(max(m, 0))}
+
     def bytes(self):
         d, m = C.c_int64(0), C.c_int64(0)
         check(lib().symmspmv_plan_bytes(self._h, C.byref(d), C.byref(m)))

@@ -48,7 +48,8 @@ EXPORTS = [
     "race_config_default", "race_build_schedule", "race_schedule_get_stats", "race_schedule_permutation",
     "race_schedule_table", "race_schedule_permuted_matrix", "race_schedule_destroy", "symmspmv_options_default",
     "symmspmv_plan", "symmspmv_plan_rows", "symmspmv_run", "symmspmv_run_variant", "symmspmv_run_host",
-    "symmspmv_last_launches", "symmspmv_plan_bytes", "symmspmv_destroy", "symm_status_string", "symm_last_error",
+    "symmspmv_last_launches", "symmspmv_plan_bytes", "symmspmv_plan_info", "symmspmv_destroy", "symm_status_string",
+    "symm_last_error",
 ]
 
 _LIB = None
@@ -78,6 +79,7 @@ def lib():
             "symmspmv_run_host": ([vp, vp, vp, vp], C.c_int),
             "symmspmv_last_launches": ([vp], C.c_int),
             "symmspmv_plan_bytes": ([vp, vp, vp], C.c_int),
+            "symmspmv_plan_info": ([vp, vp, i32], C.c_int),
             "symmspmv_destroy": ([vp], C.c_int),
             "symm_status_string": ([C.c_int], C.c_char_p),
             "symm_last_error": ([], C.c_char_p),

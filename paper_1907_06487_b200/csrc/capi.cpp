@@ -248,14 +248,16 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   A.window_cap = window_cap;
   A.nnz_cap = nnz_cap;
   P->fargs = FixupArgs{n, P->d_in_ptr, d_spill};
-  if (tiled_smem_bytes(A) > 227 * 1024)
-    return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel needs %d B of shared memory (> 227 KB)", tiled_smem_bytes(A));
-  int occ = 0;
-  rc = tiled_max_ctas_per_sm(P->vec, A, &occ);
-  if (rc) return cuda_fail((cudaError_t)rc, "occupancy query (tiled)");
-  if (occ < 1) return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel does not fit an SM");
-  P->tiled_occ = occ;
-  P->tiled_grid = std::max(1, std::min(occ * P->sms, nt));
+  int stages = 0;
+  rc = tiled_max_ctas_per_sm(P->vec, A, &stages);
+  if (rc) return cuda_fail((cudaError_t)rc, "shared-memory attribute (tiled)");
+  if (stages < 2) {
+    A.stages = 2;
+    return set_error(SYMM_ERR_UNSUPPORTED, "tiled kernel needs %d B of shared memory for 2 stages", tiled_smem_bytes(A));
+  }
+  A.stages = stages;
+  P->tiled_occ = stages;
+  P->tiled_grid = std::max(1, std::min(P->sms, nt));
   P->has_tiled = true;
   return SYMM_OK;
 }
@@ -348,7 +350,7 @@ void race_config_default(race_config* c) {
   std::memset(c, 0, sizeof *c);
   c->k = 2;
   c->n_workers = 0;
-  c->tile_work = 1280;
+  c->tile_work = 1792;
   c->balance_by = 1;
   c->root = -1;
   c->n_eps = 3;
@@ -357,7 +359,7 @@ void race_config_default(race_config* c) {
   for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
   c->max_tile_rows = 1024;
   c->max_tile_window = 768;
-  c->max_tile_nnz = 1024;
+  c->max_tile_nnz = 1536;
   c->reorder = 1;
   c->validate = 1;
   c->flags = 0;
@@ -633,6 +635,15 @@ int symmspmv_plan_bytes(const symmspmv_plan_t* p, int64_t* device_bytes, int64_t
   if (device_bytes) *device_bytes = p->device_bytes;
   if (min_bytes) *min_bytes = p->min_bytes;
   return SYMM_OK;
+}
+
+int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n) {
+  if (!p || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
+  int32_t v[8] = {p->variant, p->vec, p->tiled_grid, p->targs.stages, p->targs.block_cap, p->targs.window_cap,
+                  p->targs.nnz_cap, p->has_tiled ? tiled_smem_bytes(p->targs) : 0};
+  int32_t m = n < 8 ? n : 8;
+  for (int32_t i = 0; i < m; ++i) out[i] = v[i];
+  return m;
 }
 
 int symmspmv_destroy(symmspmv_plan_t* p) {

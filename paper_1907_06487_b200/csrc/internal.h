@@ -96,6 +96,7 @@ struct TiledArgs {
   const int32_t* targets;         // spill targets of all tiles (tile order)
   double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
+  int32_t stages;                 // smem ring depth (chosen at plan time)
 };
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions
@@ -128,7 +129,7 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream);
 int launch_fixup(const FixupArgs& F, double* y, void* stream);
 int tiled_smem_bytes(const TiledArgs& T);
-int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);
+int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);  // returns the ring depth in *out
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 int launch_scatter(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 

@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //                           (k_fixup then adds the staged values in slot order);
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
-constexpr int kStages = 8;
+constexpr int kMaxStages = 8;
 constexpr int kGroupWarps = 8;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 2;
@@ -201,17 +201,17 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
 }
 
-template <bool ATOMIC>
+template <bool ATOMIC, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char sm[];
-  __shared__ __align__(8) uint64_t blk_full[kStages], x_full[kStages], empty[kStages];
-  __shared__ __align__(16) TileDesc sdesc[kStages];
+  __shared__ __align__(8) uint64_t blk_full[NS], x_full[NS], empty[NS];
+  __shared__ __align__(16) TileDesc sdesc[NS];
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&blk_full[s], 1);
       mbar_init(&x_full[s], 32);
       mbar_init(&empty[s], 1);
@@ -221,19 +221,33 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   __syncthreads();
   if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
-    // per tile: descriptor + block + the 16-B aligned part of x[row0 .. row0+T)
-    if (lane == 0) {
-      int k = 0;
-      int t = blockIdx.x;
-      int64_t off = 0;
-      unsigned bytes = 0;
-      int row0 = 0, T = 0;
-      if (t < A.ntiles) {
-        off = A.tiles[t].block_off; bytes = (unsigned)A.tiles[t].block_bytes;
-        row0 = A.tiles[t].row0; T = A.tiles[t].nrows;
+    // per tile: descriptor + block + the 16-B aligned part of x[row0 .. row0+T).
+    // Descriptor fields are prefetched 32 tiles at a time (one per lane,
+    // double-buffered) so no global load latency sits between two issues.
+    int64_t c_off = 0, n_off = 0;
+    int c_bytes = 0, c_row0 = 0, c_T = 0, n_bytes = 0, n_row0 = 0, n_T = 0;
+    auto fetch = [&](int kb, int64_t& off, int& bytes, int& row0, int& T) {
+      const int tt = blockIdx.x + (kb + lane) * G;
+      if (tt < A.ntiles) {
+        const TileDesc& D = A.tiles[tt];
+        off = D.block_off; bytes = D.block_bytes; row0 = D.row0; T = D.nrows;
       }
-      for (; t < A.ntiles; t += G, ++k) {
-        const int s = k % kStages, use = k / kStages;
+    };
+    fetch(0, c_off, c_bytes, c_row0, c_T);
+    fetch(32, n_off, n_bytes, n_row0, n_T);
+    int k = 0;
+    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+      const int j = k & 31;
+      if (j == 0 && k > 0) {
+        c_off = n_off; c_bytes = n_bytes; c_row0 = n_row0; c_T = n_T;
+        fetch(k + 32, n_off, n_bytes, n_row0, n_T);
+      }
+      const int64_t off = __shfl_sync(0xffffffffu, c_off, j);
+      const unsigned bytes = (unsigned)__shfl_sync(0xffffffffu, c_bytes, j);
+      const int row0 = __shfl_sync(0xffffffffu, c_row0, j);
+      const int T = __shfl_sync(0xffffffffu, c_T, j);
+      if (lane == 0) {
+        const int s = k % NS, use = k / NS;
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
         const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);  // 1: x+row0 is 8 mod 16
         const int nfull = T > p ? ((T - p) & ~1) : 0;           // aligned element pairs
@@ -244,24 +258,20 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         bulk_g2s(&sdesc[s], A.tiles + t, (unsigned)sizeof(TileDesc), &blk_full[s]);
         bulk_g2s(sm + s * slot_bytes, A.blocks + off, bytes, &blk_full[s]);
         if (xbytes) bulk_g2s(xs + p, x + row0 + p, xbytes, &blk_full[s]);
-        const int tn = t + G;  // prefetch the next descriptor
-        if (tn < A.ntiles) {
-          off = A.tiles[tn].block_off; bytes = (unsigned)A.tiles[tn].block_bytes;
-          row0 = A.tiles[tn].row0; T = A.tiles[tn].nrows;
-        }
       }
+      __syncwarp();
     }
     return;
   }
   if (wid == kGroups * kGroupWarps + 1) {
     // ------------------------------------------------ gather warp (x window)
-    // waits for the tile block (the loader runs kStages tiles ahead, so it has
+    // waits for the tile block (the loader runs NS tiles ahead, so it has
     // usually landed), reads the spill targets from shared memory and issues
     // the x gathers: no global-latency chain per tile.
     int k = 0;
     for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
-      const int s = k % kStages;
-      mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));
+      const int s = k % NS;
+      mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));
       const TileDesc& D = sdesc[s];
       const int row0 = D.row0, T = D.nrows, S = D.nspill;
       const unsigned char* blk = sm + s * slot_bytes;
@@ -281,12 +291,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // -------------------------------------------------- consumer groups
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
-  double2* PQ = reinterpret_cast<double2*>(sm + kStages * slot_bytes) + (size_t)g * A.nnz_cap;
+  double2* PQ = reinterpret_cast<double2*>(sm + NS * slot_bytes) + (size_t)g * A.nnz_cap;
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
-    const int s = k % kStages;
-    mbar_wait(&blk_full[s], (unsigned)((k / kStages) & 1));  // TMA data visible to this thread
-    mbar_wait(&x_full[s], (unsigned)((k / kStages) & 1));
+    const int s = k % NS;
+    mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));  // TMA data visible to this thread
+    mbar_wait(&x_full[s], (unsigned)((k / NS) & 1));
     const TileDesc& D = sdesc[s];
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
     const unsigned char* blk = sm + s * slot_bytes;
@@ -405,18 +415,42 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 }
 
 int tiled_smem_bytes(const TiledArgs& T) {
-  return kStages * (T.block_cap + 8 * T.window_cap) + kGroups * 16 * T.nnz_cap;
+  return T.stages * (T.block_cap + 8 * T.window_cap) + kGroups * 16 * T.nnz_cap;
 }
 
-int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out) {
-  (void)vec;
-  const int smem = tiled_smem_bytes(T);
-  int rc = (int)cudaFuncSetAttribute(k_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (!rc) rc = (int)cudaFuncSetAttribute(k_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int occ = 0;
-  if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<false>, kTiledThreads, smem);
-  *out = occ;
+template <int NS>
+static int tiled_attr(int smem) {
+  int rc = (int)cudaFuncSetAttribute(k_tiled<false, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (!rc) rc = (int)cudaFuncSetAttribute(k_tiled<true, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   return rc;
+}
+
+// Deepest ring (8, 6, 5, 4, 3 or 2 stages) whose shared memory fits one SM.
+int tiled_max_ctas_per_sm(int vec, const TiledArgs& T0, int* out) {
+  (void)vec;
+  TiledArgs T = T0;
+  int devsmem = 0;
+  cudaDeviceGetAttribute(&devsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+  const int cand[] = {8, 6, 5, 4, 3, 2};
+  for (int ns : cand) {
+    T.stages = ns;
+    const int smem = tiled_smem_bytes(T);
+    if (smem + 1024 > devsmem) continue;
+    int rc = 0;
+    switch (ns) {
+      case 8: rc = tiled_attr<8>(smem); break;
+      case 6: rc = tiled_attr<6>(smem); break;
+      case 5: rc = tiled_attr<5>(smem); break;
+      case 4: rc = tiled_attr<4>(smem); break;
+      case 3: rc = tiled_attr<3>(smem); break;
+      default: rc = tiled_attr<2>(smem); break;
+    }
+    if (rc) return rc;
+    *out = ns;
+    return 0;
+  }
+  *out = 0;
+  return 0;
 }
 
 int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream) {
@@ -424,8 +458,16 @@ int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int gr
   if (T.ntiles <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = tiled_smem_bytes(T);
-  if (atomic_flush) k_tiled<true><<<grid, kTiledThreads, smem, st>>>(T, x, y);
-  else k_tiled<false><<<grid, kTiledThreads, smem, st>>>(T, x, y);
+#define LT(NSV)                                                                             \
+  case NSV:                                                                                 \
+    if (atomic_flush) k_tiled<true, NSV><<<grid, kTiledThreads, smem, st>>>(T, x, y);       \
+    else k_tiled<false, NSV><<<grid, kTiledThreads, smem, st>>>(T, x, y);                   \
+    break;
+  switch (T.stages) {
+    LT(8) LT(6) LT(5) LT(4) LT(3) LT(2)
+    default: return (int)cudaErrorInvalidValue;
+  }
+#undef LT
   return (int)cudaGetLastError();
 }
 
