@@ -136,7 +136,8 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     for (int32_t r = r0; r < r1; ++r)
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
     const int64_t W = (int64_t)T + S_;
-    int64_t o_lcol = align16(2 * (int64_t)(T + 1));
+    const int64_t o_start = (int64_t)sizeof(TileDesc);
+    int64_t o_lcol = align16(o_start + 2 * (int64_t)(T + 1));
     int64_t o_tidx = align16(o_lcol + 4 * nnz);
     int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
     int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
@@ -185,7 +186,8 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     const int32_t r0 = D.row0, T = D.nrows, r1 = r0 + T, ns = D.nspill, W = T + ns;
     const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
     unsigned char* blk = blocks.data() + D.block_off;
-    uint16_t* start = reinterpret_cast<uint16_t*>(blk);
+    std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
+    uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
     uint32_t* rcol = reinterpret_cast<uint32_t*>(blk + D.o_lcol);
     uint16_t* tidx = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
@@ -635,6 +637,24 @@ int symmspmv_plan_bytes(const symmspmv_plan_t* p, int64_t* device_bytes, int64_t
   if (device_bytes) *device_bytes = p->device_bytes;
   if (min_bytes) *min_bytes = p->min_bytes;
   return SYMM_OK;
+}
+
+// Diagnostics (not in the public header): run the tiled kernel once with the
+// event trace of CTA 0 enabled; copies up to `cap` tiles x 8 timestamps to host.
+extern "C" int symmspmv_debug_trace(symmspmv_plan_t* P, const double* x, double* y, void* stream,
+                                    unsigned long long* host_trace, int32_t cap) {
+  if (!P || !P->has_tiled) return set_error(SYMM_ERR_ARG, "no tiled plan");
+  unsigned long long* d = nullptr;
+  size_t bytes = (size_t)cap * 8 * sizeof(unsigned long long);
+  if (cudaMalloc(&d, bytes) != cudaSuccess) return set_error(SYMM_ERR_OOM, "trace buffer");
+  cudaMemset(d, 0, bytes);
+  TiledArgs A = P->targs;
+  A.trace = d;
+  int rc = launch_tiled(A, x, y, P->vec, P->tiled_grid, false, stream);
+  cudaStreamSynchronize((cudaStream_t)stream);
+  cudaMemcpy(host_trace, d, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return rc ? cuda_fail((cudaError_t)rc, "trace launch") : SYMM_OK;
 }
 
 int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n) {

@@ -68,7 +68,7 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
-//   start u16[T+1] | rc u32[nnz] | tidx u16[noff] | tptr u16[W+1] |
+//   TileDesc (64 B) | start u16[T+1] | rc u32[nnz] | tidx u16[noff] | tptr u16[W+1] |
 //   tgt i32[S] | slot i32[S] | val f64[nnz]
 // rc[e] = (local row << 16) | local column of entry e
 // (tgt is also kept in the global `targets` array for the x-gather warp)
@@ -83,7 +83,7 @@ struct TileDesc {
   int32_t nspill;       // S (window W = T + S)
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
-  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block
+  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block (start at 64)
   int32_t spill_off;    // first spill target of this tile in `targets`
   int32_t pad[5];
 };
@@ -97,6 +97,7 @@ struct TiledArgs {
   double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)
+  unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
 };
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions

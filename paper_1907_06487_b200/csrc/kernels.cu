@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 constexpr int kMaxStages = 8;
 constexpr int kGroupWarps = 8;
 constexpr int kGroupThreads = kGroupWarps * 32;
-constexpr int kGroups = 2;
+constexpr int kGroups = 3;
 constexpr int kTiledThreads = kGroups * kGroupThreads + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -197,6 +197,19 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace layout (CTA 0 only): 8 slots per local tile k
+//   0 loader issue, 1 gather saw block, 2 gather issued, 3 consumer got x,
+//   4 pass A done, 5 pass B done, 6 group id
+#define TRACE(k, slot)                                                               \
+  do {                                                                               \
+    if (A.trace != nullptr && blockIdx.x == 0) A.trace[(size_t)(k) * 8 + (slot)] = gtimer(); \
+  } while (0)
+
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
 }
@@ -206,7 +219,6 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
                                                             double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t blk_full[NS], x_full[NS], empty[NS];
-  __shared__ __align__(16) TileDesc sdesc[NS];
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
@@ -225,39 +237,33 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // Descriptor fields are prefetched 32 tiles at a time (one per lane,
     // double-buffered) so no global load latency sits between two issues.
     int64_t c_off = 0, n_off = 0;
-    int c_bytes = 0, c_row0 = 0, c_T = 0, n_bytes = 0, n_row0 = 0, n_T = 0;
-    auto fetch = [&](int kb, int64_t& off, int& bytes, int& row0, int& T) {
+    int c_bytes = 0, n_bytes = 0;
+    auto fetch = [&](int kb, int64_t& off, int& bytes) {
       const int tt = blockIdx.x + (kb + lane) * G;
       if (tt < A.ntiles) {
-        const TileDesc& D = A.tiles[tt];
-        off = D.block_off; bytes = D.block_bytes; row0 = D.row0; T = D.nrows;
+        off = A.tiles[tt].block_off;
+        bytes = A.tiles[tt].block_bytes;
       }
     };
-    fetch(0, c_off, c_bytes, c_row0, c_T);
-    fetch(32, n_off, n_bytes, n_row0, n_T);
+    fetch(0, c_off, c_bytes);
+    fetch(32, n_off, n_bytes);
     int k = 0;
     for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
       const int j = k & 31;
       if (j == 0 && k > 0) {
-        c_off = n_off; c_bytes = n_bytes; c_row0 = n_row0; c_T = n_T;
-        fetch(k + 32, n_off, n_bytes, n_row0, n_T);
+        c_off = n_off; c_bytes = n_bytes;
+        fetch(k + 32, n_off, n_bytes);
       }
       const int64_t off = __shfl_sync(0xffffffffu, c_off, j);
       const unsigned bytes = (unsigned)__shfl_sync(0xffffffffu, c_bytes, j);
-      const int row0 = __shfl_sync(0xffffffffu, c_row0, j);
-      const int T = __shfl_sync(0xffffffffu, c_T, j);
       if (lane == 0) {
         const int s = k % NS, use = k / NS;
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
-        const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);  // 1: x+row0 is 8 mod 16
-        const int nfull = T > p ? ((T - p) & ~1) : 0;           // aligned element pairs
-        const unsigned xbytes = (unsigned)nfull * 8u;
-        double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&blk_full[s], bytes + (unsigned)sizeof(TileDesc) + xbytes);
-        bulk_g2s(&sdesc[s], A.tiles + t, (unsigned)sizeof(TileDesc), &blk_full[s]);
+        // one bulk copy per tile (descriptor + block): the issue cost of
+        // cp.async.bulk (~130 ns, measured) is paid once per tile
+        mbar_arrive_expect_tx(&blk_full[s], bytes);
         bulk_g2s(sm + s * slot_bytes, A.blocks + off, bytes, &blk_full[s]);
-        if (xbytes) bulk_g2s(xs + p, x + row0 + p, xbytes, &blk_full[s]);
+        TRACE(k, 0);
       }
       __syncwarp();
     }
@@ -272,36 +278,38 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
       const int s = k % NS;
       mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));
-      const TileDesc& D = sdesc[s];
-      const int row0 = D.row0, T = D.nrows, S = D.nspill;
+      if (lane == 0) TRACE(k, 1);
       const unsigned char* blk = sm + s * slot_bytes;
+      const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
+      const int row0 = D.row0, T = D.nrows, S = D.nspill;
       const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
-      const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
-      const int nfull = T > p ? ((T - p) & ~1) : 0;
-      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
-      // own elements outside the bulk-copied aligned range: [0, p) and [p + nfull, T)
-      if (lane == 0 && p == 1) cp_async8(xs, x + row0);
-      if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
+      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap);
+      const double* xo = x + row0;
+#pragma unroll 4
+      for (int i = lane; i < T; i += 32) cp_async8(xs + i, xo + i);
 #pragma unroll 4
       for (int idx = lane; idx < S; idx += 32) cp_async8(xs + T + idx, x + tgt[idx]);
       cp_async_arrive_noinc(&x_full[s]);
+      if (lane == 0) TRACE(k, 2);
     }
     return;
   }
   // -------------------------------------------------- consumer groups
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
-  double2* PQ = reinterpret_cast<double2*>(sm + NS * slot_bytes) + (size_t)g * A.nnz_cap;
+  double* Pp = reinterpret_cast<double*>(sm + NS * slot_bytes) + (size_t)g * 2 * A.nnz_cap;
+  double* Qp = Pp + A.nnz_cap;
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
     mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));  // TMA data visible to this thread
     mbar_wait(&x_full[s], (unsigned)((k / NS) & 1));
-    const TileDesc& D = sdesc[s];
-    const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
+    if (gt == 0) TRACE(k, 3);
     const unsigned char* blk = sm + s * slot_bytes;
-    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
-    const uint16_t* start = reinterpret_cast<const uint16_t*>(blk);
+    const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
+    const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
+    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap);
+    const uint16_t* start = reinterpret_cast<const uint16_t*>(blk + sizeof(TileDesc));
     const uint32_t* rcol = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
     const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
@@ -313,9 +321,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     for (int e = gt; e < nnz; e += kGroupThreads) {
       const uint32_t rc = rcol[e];
       const double a = val[e];
-      PQ[e] = make_double2(a * xs[rc >> 16], a * xs[rc & 0xffffu]);
+      Pp[e] = a * xs[rc >> 16];
+      Qp[e] = a * xs[rc & 0xffffu];
     }
     group_sync(g);
+    if (gt == 0) TRACE(k, 4);
     // pass B: one thread per local target: own row sum (tmp)
     // + transposed contributions, fixed order; then the flush
     for (int l = gt; l < W; l += kGroupThreads) {
@@ -323,11 +333,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       if (l < T) {
         const int eb = start[l], ee = start[l + 1];
 #pragma unroll 4
-        for (int e = eb; e < ee; ++e) acc += PQ[e].y;
+        for (int e = eb; e < ee; ++e) acc += Qp[e];
       }
       const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
-      for (int j = jb; j < je; ++j) acc += PQ[tidx[j]].x;
+      for (int j = jb; j < je; ++j) acc += Pp[tidx[j]];
       if (ATOMIC) {
         atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
       } else if (l < T) {
@@ -337,7 +347,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       }
     }
     group_sync(g);  // stage s and this group's PQ are free again
-    if (gt == 0) mbar_arrive(&empty[s]);
+    if (gt == 0) {
+      mbar_arrive(&empty[s]);
+      TRACE(k, 5);
+      if (A.trace != nullptr && blockIdx.x == 0) A.trace[(size_t)k * 8 + 6] = (unsigned long long)g;
+    }
   }
 }
 
