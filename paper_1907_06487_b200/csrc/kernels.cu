@@ -149,19 +149,19 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //                 blk_full[s] (after the stage was released: empty[s]);
 //   gather warp:  when a block has landed, cp.async-gathers x of the tile
 //                 window (own rows + spill targets) -> x_full[s];
-//   2 consumer groups x 8 warps, alternating tiles (their passes overlap):
-//     pass A (entry-parallel):        PQ[e] = (a_e x[r_e], a_e x[c_e])
-//     pass B (thread per target l):   y_l = sum_{e in row l} Q[e]            (tmp)
-//                                         + sum_{e: c_e = l, e off-diag} P[e]
-//     both conflict-free, fixed order -> deterministic; pass B flushes:
+//   kGroups consumer groups x kGroupWarps warps, round-robin over the tiles
+//   of the CTA (several tiles in flight per SM); one pass, thread per target l:
+//     y_l = sum_{e in row l} a_e x[c_e]                      (tmp)
+//         + sum_{e: c_e = l, e off-diagonal} a_e x[r_e]      (b[col] += ...)
+//     fixed order -> deterministic; the result is flushed:
 //       K3 (deterministic): own rows -> y (store), spill -> spill_buf[slot]
 //                           (k_fixup then adds the staged values in slot order);
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
 constexpr int kMaxStages = 8;
-constexpr int kGroupWarps = 8;
+constexpr int kGroupWarps = 6;
 constexpr int kGroupThreads = kGroupWarps * 32;
-constexpr int kGroups = 3;
+constexpr int kGroups = 4;
 constexpr int kTiledThreads = kGroups * kGroupThreads + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -172,6 +172,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -226,46 +229,54 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     for (int s = 0; s < NS; ++s) {
       mbar_init(&blk_full[s], 1);
       mbar_init(&x_full[s], 32);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kGroupWarps);  // every consumer warp of the group arrives
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
-    // per tile: descriptor + block + the 16-B aligned part of x[row0 .. row0+T).
-    // Descriptor fields are prefetched 32 tiles at a time (one per lane,
-    // double-buffered) so no global load latency sits between two issues.
-    int64_t c_off = 0, n_off = 0;
-    int c_bytes = 0, n_bytes = 0;
-    auto fetch = [&](int kb, int64_t& off, int& bytes) {
-      const int tt = blockIdx.x + (kb + lane) * G;
-      if (tt < A.ntiles) {
-        off = A.tiles[tt].block_off;
-        bytes = A.tiles[tt].block_bytes;
-      }
-    };
-    fetch(0, c_off, c_bytes);
-    fetch(32, n_off, n_bytes);
-    int k = 0;
-    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
-      const int j = k & 31;
-      if (j == 0 && k > 0) {
-        c_off = n_off; c_bytes = n_bytes;
-        fetch(k + 32, n_off, n_bytes);
-      }
-      const int64_t off = __shfl_sync(0xffffffffu, c_off, j);
-      const unsigned bytes = (unsigned)__shfl_sync(0xffffffffu, c_bytes, j);
-      if (lane == 0) {
+    // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
+    // register ring (loop unrolled by 4) so each issue finds its operands ready.
+    if (lane == 0) {
+      int64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+      int b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+      auto ld = [&](int kk, int64_t& o, int& bb) {
+        const int tt = blockIdx.x + kk * G;
+        if (tt < A.ntiles) {
+          o = A.tiles[tt].block_off;
+          bb = A.tiles[tt].block_bytes;
+        }
+      };
+      auto issue = [&](int k, int64_t off, int bytes) {
         const int s = k % NS, use = k / NS;
+        TRACE(k, 6);
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
+        TRACE(k, 7);
         // one bulk copy per tile (descriptor + block): the issue cost of
         // cp.async.bulk (~130 ns, measured) is paid once per tile
-        mbar_arrive_expect_tx(&blk_full[s], bytes);
-        bulk_g2s(sm + s * slot_bytes, A.blocks + off, bytes, &blk_full[s]);
+        mbar_arrive_expect_tx(&blk_full[s], (unsigned)bytes);
+        bulk_g2s(sm + s * slot_bytes, A.blocks + off, (unsigned)bytes, &blk_full[s]);
         TRACE(k, 0);
+      };
+      ld(0, o0, b0);
+      ld(1, o1, b1);
+      ld(2, o2, b2);
+      ld(3, o3, b3);
+      const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
+      for (int kb = 0; kb < nk; kb += 4) {
+        issue(kb, o0, b0);
+        ld(kb + 4, o0, b0);
+        if (kb + 1 >= nk) break;
+        issue(kb + 1, o1, b1);
+        ld(kb + 5, o1, b1);
+        if (kb + 2 >= nk) break;
+        issue(kb + 2, o2, b2);
+        ld(kb + 6, o2, b2);
+        if (kb + 3 >= nk) break;
+        issue(kb + 3, o3, b3);
+        ld(kb + 7, o3, b3);
       }
-      __syncwarp();
     }
     return;
   }
@@ -297,8 +308,6 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // -------------------------------------------------- consumer groups
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
-  double* Pp = reinterpret_cast<double*>(sm + NS * slot_bytes) + (size_t)g * 2 * A.nnz_cap;
-  double* Qp = Pp + A.nnz_cap;
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
@@ -316,28 +325,22 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = reinterpret_cast<const int32_t*>(blk + D.o_slot);
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    const int nnz = D.nnz;
-    // pass A: entry-parallel products  PQ[e] = (a_e x[row_e], a_e x[col_e])
-    for (int e = gt; e < nnz; e += kGroupThreads) {
-      const uint32_t rc = rcol[e];
-      const double a = val[e];
-      Pp[e] = a * xs[rc >> 16];
-      Qp[e] = a * xs[rc & 0xffffu];
-    }
-    group_sync(g);
-    if (gt == 0) TRACE(k, 4);
-    // pass B: one thread per local target: own row sum (tmp)
-    // + transposed contributions, fixed order; then the flush
+    // one pass, one thread per local target l (fixed order -> deterministic):
+    //   own row l:  sum_{e in row l} a_e x[c_e]                    (tmp)
+    //   every l:    sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
     for (int l = gt; l < W; l += kGroupThreads) {
       double acc = 0.0;
       if (l < T) {
         const int eb = start[l], ee = start[l + 1];
 #pragma unroll 4
-        for (int e = eb; e < ee; ++e) acc += Qp[e];
+        for (int e = eb; e < ee; ++e) acc += val[e] * xs[rcol[e] & 0xffffu];
       }
       const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
-      for (int j = jb; j < je; ++j) acc += Pp[tidx[j]];
+      for (int j = jb; j < je; ++j) {
+        const int e = tidx[j];
+        acc += val[e] * xs[rcol[e] >> 16];
+      }
       if (ATOMIC) {
         atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
       } else if (l < T) {
@@ -346,12 +349,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         __stcg(A.spill_buf + slot[l - T], acc);
       }
     }
-    group_sync(g);  // stage s and this group's PQ are free again
-    if (gt == 0) {
-      mbar_arrive(&empty[s]);
-      TRACE(k, 5);
-      if (A.trace != nullptr && blockIdx.x == 0) A.trace[(size_t)k * 8 + 6] = (unsigned long long)g;
-    }
+    if (gt == 0) TRACE(k, 4);
+    // release stage s: each warp arrives once its reads of the stage are done
+    __syncwarp();
+    if (lane == 0) mbar_arrive_relaxed(&empty[s]);
+    if (gt == 0) TRACE(k, 5);
   }
 }
 
@@ -429,7 +431,7 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 }
 
 int tiled_smem_bytes(const TiledArgs& T) {
-  return T.stages * (T.block_cap + 8 * T.window_cap) + kGroups * 16 * T.nnz_cap;
+  return T.stages * (T.block_cap + 8 * T.window_cap);
 }
 
 template <int NS>

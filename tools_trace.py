@@ -44,13 +44,14 @@ span = tr[:, 5].max() - t0
 print("CTA0 span ns", span, "per tile", span / n)
 print("issue interval median", np.median(np.diff(tr[:, 0])), "consumer end interval", np.median(np.diff(np.sort(tr[:, 5]))))
 for i in list(range(0, 12)) + list(range(n // 2, n // 2 + 8)):
-    print(i, [int(v - t0) for v in tr[i, :6]], int(tr[i, 6]))
+    print(i, [int(v - t0) for v in tr[i, :8]])
 NS = plan.info()["tiled_stages"]
 gap = tr[NS:, 0] - tr[:-NS, 5]
 print("issue[k] - end[k-NS]: median", np.median(gap), "p10", np.percentile(gap, 10), "p90", np.percentile(gap, 90))
 # consumer idle: time a group waits for its next tile's x
-for g in (0, 1):
-    idx = np.where(tr[:, 6] == g)[0]
+print("loader: before-wait -> after-wait median", np.median(tr[:, 7] - tr[:, 6]), " after-wait -> issued median", np.median(tr[:, 0] - tr[:, 7]), " issued -> next before-wait", np.median(tr[1:, 6] - tr[:-1, 0]))
+for g in range(3):
+    idx = np.arange(g, n, 3)
     idle = tr[idx[1:], 3] - tr[idx[:-1], 5]
     busy = tr[idx, 5] - tr[idx, 3]
     print(f"group {g}: busy median {np.median(busy):.0f} ns, idle-before-next median {np.median(idle):.0f} ns")
