@@ -162,7 +162,8 @@ constexpr int kMaxStages = 8;
 constexpr int kGroupWarps = 6;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 4;
-constexpr int kTiledThreads = kGroups * kGroupThreads + 64;
+constexpr int kGatherWarps = 2;
+constexpr int kTiledThreads = kGroups * kGroupThreads + 32 * (1 + kGatherWarps);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -239,54 +240,64 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
     // register ring (loop unrolled by 4) so each issue finds its operands ready.
     if (lane == 0) {
-      int64_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
-      int b0 = 0, b1 = 0, b2 = 0, b3 = 0;
-      auto ld = [&](int kk, int64_t& o, int& bb) {
+      int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
+      int T0 = 0, T1 = 0, T2 = 0, T3 = 0;
+      auto ld = [&](int kk, int4& d, int& T) {
         const int tt = blockIdx.x + kk * G;
         if (tt < A.ntiles) {
-          o = A.tiles[tt].block_off;
-          bb = A.tiles[tt].block_bytes;
+          const TileDesc& D = A.tiles[tt];
+          const int64_t o = D.block_off;
+          d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
+          T = D.nrows;
         }
       };
-      auto issue = [&](int k, int64_t off, int bytes) {
+      auto issue = [&](int k, int4 d, int T) {
         const int s = k % NS, use = k / NS;
+        const int64_t off = (int64_t)(uint32_t)d.x | ((int64_t)d.y << 32);
+        const int row0 = d.w;
+        // 16-B aligned part of x[row0 .. row0+T) by TMA too; the gather warps
+        // add the (at most two) unaligned edge elements and the spill targets
+        const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
+        const int nfull = T > p ? ((T - p) & ~1) : 0;
+        const unsigned xbytes = (unsigned)nfull * 8u;
         TRACE(k, 6);
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
         TRACE(k, 7);
-        // one bulk copy per tile (descriptor + block): the issue cost of
-        // cp.async.bulk (~130 ns, measured) is paid once per tile
-        mbar_arrive_expect_tx(&blk_full[s], (unsigned)bytes);
-        bulk_g2s(sm + s * slot_bytes, A.blocks + off, (unsigned)bytes, &blk_full[s]);
+        double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
+        mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z + xbytes);
+        bulk_g2s(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s]);
+        if (xbytes) bulk_g2s(xs + p, x + row0 + p, xbytes, &blk_full[s]);
         TRACE(k, 0);
       };
-      ld(0, o0, b0);
-      ld(1, o1, b1);
-      ld(2, o2, b2);
-      ld(3, o3, b3);
+      ld(0, d0, T0);
+      ld(1, d1, T1);
+      ld(2, d2, T2);
+      ld(3, d3, T3);
       const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
       for (int kb = 0; kb < nk; kb += 4) {
-        issue(kb, o0, b0);
-        ld(kb + 4, o0, b0);
+        issue(kb, d0, T0);
+        ld(kb + 4, d0, T0);
         if (kb + 1 >= nk) break;
-        issue(kb + 1, o1, b1);
-        ld(kb + 5, o1, b1);
+        issue(kb + 1, d1, T1);
+        ld(kb + 5, d1, T1);
         if (kb + 2 >= nk) break;
-        issue(kb + 2, o2, b2);
-        ld(kb + 6, o2, b2);
+        issue(kb + 2, d2, T2);
+        ld(kb + 6, d2, T2);
         if (kb + 3 >= nk) break;
-        issue(kb + 3, o3, b3);
-        ld(kb + 7, o3, b3);
+        issue(kb + 3, d3, T3);
+        ld(kb + 7, d3, T3);
       }
     }
     return;
   }
-  if (wid == kGroups * kGroupWarps + 1) {
-    // ------------------------------------------------ gather warp (x window)
-    // waits for the tile block (the loader runs NS tiles ahead, so it has
-    // usually landed), reads the spill targets from shared memory and issues
-    // the x gathers: no global-latency chain per tile.
-    int k = 0;
-    for (int t = blockIdx.x; t < A.ntiles; t += G, ++k) {
+  if (wid >= kGroups * kGroupWarps + 1) {
+    // ------------------------------------------------ gather warps (x window)
+    // kGatherWarps warps take the tiles of this CTA in turn; each waits for its
+    // tile's block (the loader runs ahead), then cp.async-gathers the spill
+    // targets (read from shared memory) and the unaligned own-x edge elements.
+    const int gw = wid - (kGroups * kGroupWarps + 1);
+    int k = gw;
+    for (int t = blockIdx.x + gw * G; t < A.ntiles; t += kGatherWarps * G, k += kGatherWarps) {
       const int s = k % NS;
       mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));
       if (lane == 0) TRACE(k, 1);
@@ -294,10 +305,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
       const int row0 = D.row0, T = D.nrows, S = D.nspill;
       const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
-      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap);
-      const double* xo = x + row0;
-#pragma unroll 4
-      for (int i = lane; i < T; i += 32) cp_async8(xs + i, xo + i);
+      const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
+      const int nfull = T > p ? ((T - p) & ~1) : 0;
+      double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
+      if (lane == 0 && p == 1) cp_async8(xs, x + row0);
+      if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
 #pragma unroll 4
       for (int idx = lane; idx < S; idx += 32) cp_async8(xs + T + idx, x + tgt[idx]);
       cp_async_arrive_noinc(&x_full[s]);
@@ -317,7 +329,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const unsigned char* blk = sm + s * slot_bytes;
     const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
-    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap);
+    const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk + sizeof(TileDesc));
     const uint32_t* rcol = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
     const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
