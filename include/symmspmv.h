@@ -126,7 +126,7 @@ void race_schedule_destroy(race_schedule_t* s);
 
 /* ---- execution ---------------------------------------------------------- */
 typedef enum {
-  SYMM_VARIANT_AUTO = 0,    /* tiled if every tile fits, else colored                 */
+  SYMM_VARIANT_AUTO = 0,    /* tiled_atomic if every tile fits, else colored          */
   SYMM_VARIANT_COLORED = 1, /* K2: one launch per phase, global read-modify-write     */
   SYMM_VARIANT_ATOMIC = 2,  /* K1: one launch, native fp64 RED for transposed updates */
   SYMM_VARIANT_TILED = 3,   /* K3: TMA-staged tiles, smem two-pass, staged fixup; deterministic */

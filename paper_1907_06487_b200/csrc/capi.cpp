@@ -289,7 +289,8 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
   P->last_launches = 0;
   if (P->n == 0) return SYMM_OK;
   if (variant == SYMM_VARIANT_AUTO) variant = P->variant;
-  if (variant == SYMM_VARIANT_AUTO) variant = P->has_tiled ? SYMM_VARIANT_TILED : SYMM_VARIANT_COLORED;
+  // AUTO: the fastest measured variant (profiles/) that this plan holds
+  if (variant == SYMM_VARIANT_AUTO) variant = P->has_tiled ? SYMM_VARIANT_TILED_ATOMIC : SYMM_VARIANT_COLORED;
   if (variant == SYMM_VARIANT_ATOMIC) {
     if (!P->has_csr) return set_error(SYMM_ERR_ARG, "variant ATOMIC was not uploaded by this plan");
     CsrArgs A{P->n, P->d_rp, P->d_col, P->d_val};
