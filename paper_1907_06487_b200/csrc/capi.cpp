@@ -138,11 +138,11 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     const int64_t W = (int64_t)T + S_;
     const int64_t o_start = (int64_t)sizeof(TileDesc);
     int64_t o_lcol = align16(o_start + 2 * (int64_t)(T + 1));
-    int64_t o_tidx = align16(o_lcol + 4 * nnz);
-    int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
+    int64_t o_tidx = align16(o_lcol + 2 * nnz);
+    int64_t o_tptr = align16(o_tidx + 4 * (nnz - nd));
     int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
-    int64_t o_slot = align16(o_tgt + 4 * (int64_t)S_);
-    int64_t o_val = align16(o_slot + 4 * (int64_t)S_);
+    int64_t o_slot = o_tgt;
+    int64_t o_val = align16(o_tgt + 4 * (int64_t)S_);
     int64_t bytes = align16(o_val + 8 * nnz);
     if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
     TileDesc& D = desc[(size_t)t];
@@ -188,16 +188,12 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     unsigned char* blk = blocks.data() + D.block_off;
     std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
     uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
-    uint32_t* rcol = reinterpret_cast<uint32_t*>(blk + D.o_lcol);
-    uint16_t* tidx = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
+    uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
+    uint32_t* tcsc = reinterpret_cast<uint32_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
-    int32_t* slt = reinterpret_cast<int32_t*>(blk + D.o_slot);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
-    for (int32_t j = 0; j < ns; ++j) {
-      tgt[j] = (int32_t)((uint32_t)sp[j] & kIdxMask);
-      slt[j] = slots[(size_t)(S.spill_ptr[(size_t)t] + j)];
-    }
+    for (int32_t j = 0; j < ns; ++j) tgt[j] = (int32_t)((uint32_t)sp[j] & kIdxMask);
     const int32_t e0 = S.prow_ptr[(size_t)r0];
     std::vector<int32_t> tcnt((size_t)W + 1, 0);
     for (int32_t r = r0; r < r1; ++r) {
@@ -216,7 +212,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
           if (lo >= ns || tgt[lo] != c) bad |= 1;
           l = T + lo;
         }
-        rcol[i - e0] = ((uint32_t)(r - r0) << 16) | (uint32_t)l;
+        lcol[i - e0] = (uint16_t)l;
         val[i - e0] = S.pval[(size_t)i];
         if (c != r) tcnt[(size_t)l + 1]++;
       }
@@ -226,18 +222,19 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     for (int32_t l = 0; l <= W; ++l) tptr[l] = (uint16_t)tcnt[(size_t)l];
     for (int32_t r = r0; r < r1; ++r)
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
-        if (S.pcol[(size_t)i] != r) tidx[tcnt[rcol[i - e0] & 0xffffu]++] = (uint16_t)(i - e0);
+        if (S.pcol[(size_t)i] != r) tcsc[tcnt[lcol[i - e0]]++] = (uint32_t)(i - e0) | ((uint32_t)(r - r0) << 16);
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   TileDesc* d_desc;
   unsigned char* d_blocks;
   double* d_spill;
-  int32_t* d_targets;
+  int32_t *d_targets, *d_slots;
   std::vector<int32_t> targets((size_t)nsp);
   for (int64_t q = 0; q < nsp; ++q) targets[(size_t)q] = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
   int rc;
   if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
       (rc = upload(P, &d_targets, targets.data(), targets.size())) ||
+      (rc = upload(P, &d_slots, slots.data(), slots.size())) ||
       (rc = upload(P, &P->d_in_ptr, in_ptr.data(), in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)))
     return rc;
   TiledArgs& A = P->targs;
@@ -245,6 +242,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   A.ntiles = nt;
   A.blocks = d_blocks;
   A.targets = d_targets;
+  A.slots = d_slots;
   A.spill_buf = d_spill;
   A.block_cap = block_cap;
   A.window_cap = window_cap;

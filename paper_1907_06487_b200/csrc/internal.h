@@ -68,14 +68,13 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
-//   TileDesc (64 B) | start u16[T+1] | rc u32[nnz] | tidx u16[noff] | tptr u16[W+1] |
-//   tgt i32[S] | slot i32[S] | val f64[nnz]
-// rc[e] = (local row << 16) | local column of entry e
-// (tgt is also kept in the global `targets` array for the x-gather warp)
-// start: entry offsets of the T own rows (natural row order); local columns:
-// own rows 0..T-1, then spill targets T..W-1; tidx/tptr: the
-// off-diagonal entries grouped by local target (CSC of the tile); tgt: global
-// row of each spill target; slot: where K3 stages that contribution.
+//   TileDesc (64 B) | start u16[T+1] | lcol u16[nnz] | tcsc u32[noff] |
+//   tptr u16[W+1] | tgt i32[S] | val f64[nnz]
+// start: entry offsets of the T own rows (natural row order); lcol: local
+// column of each entry (own rows 0..T-1, then spill targets T..W-1);
+// tcsc/tptr: the off-diagonal entries grouped by local target (CSC of the
+// tile), each as (entry index | local row << 16); tgt: global row of each
+// spill target.  K3's staging slots live outside the block (`slots`).
 struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
@@ -83,8 +82,8 @@ struct TileDesc {
   int32_t nspill;       // S (window W = T + S)
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
-  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block (start at 64)
-  int32_t spill_off;    // first spill target of this tile in `targets`
+  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block (o_slot unused)
+  int32_t spill_off;    // first spill entry of this tile (targets / slots arrays)
   int32_t pad[5];
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
@@ -94,6 +93,7 @@ struct TiledArgs {
   int32_t ntiles;
   const unsigned char* blocks;
   const int32_t* targets;         // spill targets of all tiles (tile order)
+  const int32_t* slots;           // K3: staging slot of every spill entry (tile order)
   double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)

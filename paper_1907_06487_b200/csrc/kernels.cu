@@ -195,6 +195,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// bulk copy of data that is read exactly once per multiply (the tile blocks):
+// evict-first keeps the L2 for the x / y working set
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -240,6 +255,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
     // register ring (loop unrolled by 4) so each issue finds its operands ready.
     if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
       int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
       int T0 = 0, T1 = 0, T2 = 0, T3 = 0;
       auto ld = [&](int kk, int4& d, int& T) {
@@ -265,7 +281,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         TRACE(k, 7);
         double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
         mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z + xbytes);
-        bulk_g2s(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s]);
+        bulk_g2s_stream(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s], pol);
         if (xbytes) bulk_g2s(xs + p, x + row0 + p, xbytes, &blk_full[s]);
         TRACE(k, 0);
       };
@@ -331,11 +347,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
     const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk + sizeof(TileDesc));
-    const uint32_t* rcol = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
-    const uint16_t* tidx = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
+    const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
+    const uint32_t* tcsc = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
-    const int32_t* slot = reinterpret_cast<const int32_t*>(blk + D.o_slot);
+    const int32_t* slot = A.slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // one pass, one thread per local target l (fixed order -> deterministic):
     //   own row l:  sum_{e in row l} a_e x[c_e]                    (tmp)
@@ -345,20 +361,20 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       if (l < T) {
         const int eb = start[l], ee = start[l + 1];
 #pragma unroll 4
-        for (int e = eb; e < ee; ++e) acc += val[e] * xs[rcol[e] & 0xffffu];
+        for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
       }
       const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
       for (int j = jb; j < je; ++j) {
-        const int e = tidx[j];
-        acc += val[e] * xs[rcol[e] >> 16];
+        const uint32_t q = tcsc[j];
+        acc += val[q & 0xffffu] * xs[q >> 16];
       }
       if (ATOMIC) {
         atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
       } else if (l < T) {
         y[row0 + l] = acc;
       } else {
-        __stcg(A.spill_buf + slot[l - T], acc);
+        __stcg(A.spill_buf + __ldg(slot + (l - T)), acc);
       }
     }
     if (gt == 0) TRACE(k, 4);
