@@ -51,9 +51,15 @@ __device__ __forceinline__ double group_sum(double s) {
 
 // ---------------------------------------------------------------- zero / gather
 __global__ void k_zero(double* __restrict__ y, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // 16-B stores for the aligned body, scalar head/tail
+  const int64_t head = ((16 - ((uintptr_t)y & 15)) & 15) / 8;  // 0 or 1 element
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) y[i] = 0.0;
+  if (tid == 0 && head && n > 0) y[0] = 0.0;
+  const int64_t body = n > head ? (n - head) / 2 : 0;
+  double2* y2 = reinterpret_cast<double2*>(y + head);
+  for (int64_t i = tid; i < body; i += stride) y2[i] = make_double2(0.0, 0.0);
+  if (tid == 0 && head + 2 * body < n) y[n - 1] = 0.0;
 }
 
 __global__ void k_gather(const double* __restrict__ src, const int32_t* __restrict__ idx, double* __restrict__ dst,
@@ -357,6 +363,8 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     //   own row l:  sum_{e in row l} a_e x[c_e]                    (tmp)
     //   every l:    sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
     for (int l = gt; l < W; l += kGroupThreads) {
+      // K3: the staging slot is fetched first so its latency overlaps the sums
+      const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
       double acc = 0.0;
       if (l < T) {
         const int eb = start[l], ee = start[l + 1];
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       } else if (l < T) {
         y[row0 + l] = acc;
       } else {
-        __stcg(A.spill_buf + __ldg(slot + (l - T)), acc);
+        __stcg(A.spill_buf + sl, acc);
       }
     }
     if (gt == 0) TRACE(k, 4);
@@ -409,7 +417,7 @@ int grid_for(int64_t work, int threads) {
 
 int launch_zero(double* y, int64_t n, void* stream) {
   if (n <= 0) return 0;
-  k_zero<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(y, n);
+  k_zero<<<grid_for((n + 1) / 2, 256), 256, 0, (cudaStream_t)stream>>>(y, n);
   return (int)cudaGetLastError();
 }
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream) {
