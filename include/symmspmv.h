@@ -124,6 +124,15 @@ int race_schedule_table(const race_schedule_t* s, const char* which, int64_t* le
 int race_schedule_permuted_matrix(const race_schedule_t* s, int32_t* row_ptr, int32_t* col, double* val);
 void race_schedule_destroy(race_schedule_t* s);
 
+/* Multi-GPU row-block split of the permuted order (R23):
+ * whole tiles are assigned to ranks contiguously, balanced by stored
+ * nonzeros.  row_bounds[nranks+1] (HOST, caller-allocated): rank r owns rows
+ * [row_bounds[r], row_bounds[r+1]).  halo_end[nranks]: rank r's tiles read x
+ * and write y only inside [row_bounds[r], halo_end[r]) (halo_end[r] >=
+ * row_bounds[r+1]; every stored entry points forward, c >= r, so the halo
+ * lies in later ranks).  Either output may be NULL. */
+int race_schedule_partition(const race_schedule_t* s, int32_t nranks, int32_t* row_bounds, int32_t* halo_end);
+
 /* ---- execution ---------------------------------------------------------- */
 typedef enum {
   SYMM_VARIANT_AUTO = 0,    /* tiled_atomic if every tile fits, else colored          */
@@ -157,6 +166,19 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
 
 /* This rank's row slice [row_begin, row_end) of the permuted order. */
 int symmspmv_plan_rows(const symmspmv_plan_t* p, int32_t* row_begin, int32_t* row_end);
+
+/* Rows covered by the x / y vectors symmspmv_run expects on this rank:
+ * [row_begin, local_end) with local_end = halo_end of the partition (n for a
+ * single rank).  For nranks > 1 (variant TILED_ATOMIC only), symmspmv_run
+ * reads x over that range and writes y over it: own rows [row_begin,
+ * row_end) hold this rank's contributions, [row_end, local_end) the
+ * contributions to later ranks' rows, which the caller sends to their owners
+ * and adds (paper_1907_06487_b200/dist.py). */
+int symmspmv_plan_local(const symmspmv_plan_t* p, int32_t* row_begin, int32_t* local_end);
+
+/* y[i] += v[i], i < n (DEVICE pointers, `stream`): the owner-side add of halo
+ * contributions received from earlier ranks (SURVEY §2.5 K4 halo_add_y). */
+int symmspmv_halo_add(double* y_dev, const double* v_dev, int64_t n, void* stream);
 
 /* y := A x on `stream` (a cudaStream_t; NULL = default stream), asynchronous.
  * x_dev, y_dev: DEVICE fp64[n] in the plan's vec_order; must not overlap

@@ -76,6 +76,14 @@ class Schedule:
                                                   inv.ctypes.data_as(C.POINTER(C.c_int32))))
         return perm, inv
 
+    def partition(self, nranks: int):
+        """Row bounds [nranks+1] and halo ends [nranks] of the multi-GPU split (R23)."""
+        rb = np.empty(nranks + 1, dtype=np.int32)
+        he = np.empty(nranks, dtype=np.int32)
+        check(lib().race_schedule_partition(self._h, nranks, rb.ctypes.data_as(C.POINTER(C.c_int32)),
+                                            he.ctypes.data_as(C.POINTER(C.c_int32))))
+        return rb, he
+
     def permuted_matrix(self):
         nnz = self.stats["nnz"]
         rp = np.empty(self.n + 1, dtype=np.int32)
@@ -114,6 +122,12 @@ def build_schedule(U, **overrides) -> Schedule:
     return Schedule(h, int(U.n))
 
 
+def halo_add(y, v, stream=None):
+    """y += v on the device (C-ABI kernel), both contiguous CUDA float64 tensors."""
+    check(lib().symmspmv_halo_add(C.c_void_p(_ptr(y)), C.c_void_p(_ptr(v)), int(v.numel()),
+                                  C.c_void_p(_stream(stream))))
+
+
 def _ptr(t):
     """Device pointer of a torch CUDA float64 tensor (or a raw int)."""
     if isinstance(t, int):
@@ -139,7 +153,7 @@ class Plan:
     """symmspmv_plan_t: device-resident matrix + tables for one schedule."""
 
     def __init__(self, sched: Schedule, U=None, variant="auto", device: int = 0, vec_order="permuted",
-                 vec_width: int = 0, build_all: bool = False):
+                 vec_width: int = 0, build_all: bool = False, nranks: int = 1, rank: int = 0):
         o = _lib.SymmOptions()
         lib().symmspmv_options_default(C.byref(o))
         o.variant = VARIANTS[variant] if isinstance(variant, str) else int(variant)
@@ -147,6 +161,8 @@ class Plan:
         o.vec_order = SYMM_ORDER_ORIGINAL if vec_order == "original" else SYMM_ORDER_PERMUTED
         o.vec_width = vec_width
         o.build_all = int(build_all)
+        o.nranks = nranks
+        o.rank = rank
         h = C.c_void_p()
         if U is not None:
             s, keep = _csr_struct(U)
@@ -173,6 +189,17 @@ class Plan:
         check(lib().symmspmv_run_host(self._h, C.c_void_p(x.ctypes.data if isinstance(x, np.ndarray) else x),
                                       C.c_void_p(y.ctypes.data if isinstance(y, np.ndarray) else y),
                                       C.c_void_p(_stream(stream))))
+
+    def local_range(self):
+        """(row_begin, local_end): the rows x / y passed to run() cover."""
+        b, e = C.c_int32(0), C.c_int32(0)
+        check(lib().symmspmv_plan_local(self._h, C.byref(b), C.byref(e)))
+        return b.value, e.value
+
+    def own_rows(self):
+        b, e = C.c_int32(0), C.c_int32(0)
+        check(lib().symmspmv_plan_rows(self._h, C.byref(b), C.byref(e)))
+        return b.value, e.value
 
     @property
     def last_launches(self) -> int:

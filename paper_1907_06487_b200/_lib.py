@@ -46,8 +46,8 @@ class SymmOptions(C.Structure):
 # Every symbol include/symmspmv.h declares (tests check the export table).
 EXPORTS = [
     "race_config_default", "race_build_schedule", "race_schedule_get_stats", "race_schedule_permutation",
-    "race_schedule_table", "race_schedule_permuted_matrix", "race_schedule_destroy", "symmspmv_options_default",
-    "symmspmv_plan", "symmspmv_plan_rows", "symmspmv_run", "symmspmv_run_variant", "symmspmv_run_host",
+    "race_schedule_table", "race_schedule_permuted_matrix", "race_schedule_destroy", "race_schedule_partition",
+    "symmspmv_options_default", "symmspmv_plan", "symmspmv_plan_rows", "symmspmv_plan_local", "symmspmv_halo_add", "symmspmv_run", "symmspmv_run_variant", "symmspmv_run_host",
     "symmspmv_last_launches", "symmspmv_plan_bytes", "symmspmv_plan_info", "symmspmv_destroy", "symm_status_string",
     "symm_last_error",
 ]
@@ -71,6 +71,9 @@ def lib():
             "race_schedule_table": ([vp, C.c_char_p, vp, vp], C.c_int),
             "race_schedule_permuted_matrix": ([vp, vp, vp, vp], C.c_int),
             "race_schedule_destroy": ([vp], None),
+            "race_schedule_partition": ([vp, i32, vp, vp], C.c_int),
+            "symmspmv_plan_local": ([vp, vp, vp], C.c_int),
+            "symmspmv_halo_add": ([vp, vp, i64, vp], C.c_int),
             "symmspmv_options_default": ([vp], None),
             "symmspmv_plan": ([vp, vp, vp, vp], C.c_int),
             "symmspmv_plan_rows": ([vp, vp, vp], C.c_int),

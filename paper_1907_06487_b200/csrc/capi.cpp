@@ -40,7 +40,7 @@ struct symmspmv_plan {
   int32_t n = 0;
   int64_t nnz = 0;
   int nranks = 1, rank = 0;
-  int32_t row_begin = 0, row_end = 0;
+  int32_t row_begin = 0, row_end = 0, local_end = 0;
   std::vector<DevBuf> bufs;
   int64_t device_bytes = 0;
   // K1 / K2: permuted CRS
@@ -117,8 +117,35 @@ int pick_vec(int64_t nnz, int32_t n) {
 
 static inline int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
 
-// K3/K4 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order.
-int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
+// Contiguous tile ranges per rank, balanced by stored nonzeros (R23).
+void partition_tiles(const Schedule& S, int nranks, std::vector<int32_t>& tile_bounds,
+                     std::vector<int32_t>& row_bounds, std::vector<int32_t>& halo_end) {
+  const int32_t nt = (int32_t)S.tile_group.size();
+  tile_bounds.assign((size_t)nranks + 1, nt);
+  tile_bounds[0] = 0;
+  const int64_t total = S.nnz;
+  int64_t cum = 0;
+  int r = 1;
+  for (int32_t t = 0; t < nt && r < nranks; ++t) {
+    cum += S.prow_ptr[(size_t)S.tile_ptr[(size_t)t + 1]] - S.prow_ptr[(size_t)S.tile_ptr[(size_t)t]];
+    while (r < nranks && cum * nranks >= (int64_t)r * total) tile_bounds[(size_t)r++] = t + 1;
+  }
+  row_bounds.assign((size_t)nranks + 1, S.n);
+  halo_end.assign((size_t)nranks, S.n);
+  for (int q = 0; q <= nranks; ++q) row_bounds[(size_t)q] = nt ? S.tile_ptr[(size_t)tile_bounds[(size_t)q]] : 0;
+  row_bounds[(size_t)nranks] = S.n;
+  for (int q = 0; q < nranks; ++q) {
+    int32_t h = row_bounds[(size_t)q + 1];
+    for (int32_t t = tile_bounds[(size_t)q]; t < tile_bounds[(size_t)q + 1]; ++t)
+      if (S.spill_ptr[(size_t)t + 1] > S.spill_ptr[(size_t)t])
+        h = std::max(h, (int32_t)((uint32_t)S.spill[(size_t)S.spill_ptr[(size_t)t + 1] - 1] & kIdxMask) + 1);
+    halo_end[(size_t)q] = h;
+  }
+}
+
+// K3/K4 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order;
+// a multi-rank plan keeps only its own tile range [t_begin, t_end).
+int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t t_end) {
   const int32_t nt = (int32_t)S.tile_group.size();
   const int32_t n = S.n;
   std::vector<int32_t> tile_of((size_t)n);
@@ -225,6 +252,18 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
         if (S.pcol[(size_t)i] != r) tcsc[tcnt[lcol[i - e0]]++] = (uint32_t)(i - e0) | ((uint32_t)(r - r0) << 16);
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
+  // multi-rank: keep only this rank's tiles (descriptors re-based to the range)
+  if (t_begin != 0 || t_end != nt) {
+    const int64_t b0 = boff[(size_t)t_begin], b1 = boff[(size_t)t_end];
+    std::vector<TileDesc> d2(desc.begin() + t_begin, desc.begin() + t_end);
+    for (auto& D : d2) D.block_off -= b0;
+    std::vector<unsigned char> bl2(blocks.begin() + b0, blocks.begin() + b1);
+    for (size_t i = 0; i < d2.size(); ++i)
+      std::memcpy(bl2.data() + d2[i].block_off, &d2[i], sizeof(TileDesc));
+    desc.swap(d2);
+    blocks.swap(bl2);
+  }
+  const int32_t ntl = (int32_t)desc.size();
   TileDesc* d_desc;
   unsigned char* d_blocks;
   double* d_spill;
@@ -239,7 +278,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
     return rc;
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
-  A.ntiles = nt;
+  A.ntiles = ntl;
   A.blocks = d_blocks;
   A.targets = d_targets;
   A.slots = d_slots;
@@ -257,7 +296,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S) {
   }
   A.stages = stages;
   P->tiled_occ = stages;
-  P->tiled_grid = std::max(1, std::min(P->sms, nt));
+  P->tiled_grid = std::max(1, std::min(P->sms, ntl));
   P->has_tiled = true;
   return SYMM_OK;
 }
@@ -313,8 +352,11 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     P->last_launches = 2;
   } else if (variant == SYMM_VARIANT_TILED_ATOMIC) {
     if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED_ATOMIC was not uploaded by this plan");
-    if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
-    if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, true, st))) return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
+    // x, y cover rows [row_begin, local_end); kernels index by global row id
+    const int64_t nloc = (int64_t)P->local_end - P->row_begin;
+    if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, true, st)))
+      return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
     P->last_launches = 2;
   } else {
     return set_error(SYMM_ERR_ARG, "unknown variant %d", variant);
@@ -487,9 +529,10 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
     return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
                      (long long)U->nnz, S.n, (long long)S.nnz);
   if (opt.variant < 0 || opt.variant > 4) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
-  if (opt.nranks != 1 || opt.rank != 0)
-    return set_error(SYMM_ERR_UNSUPPORTED, "multi-rank plans are driven from Python in this version (nranks=%d)",
-                     opt.nranks);
+  if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks)
+    return set_error(SYMM_ERR_ARG, "rank %d of %d", opt.rank, opt.nranks);
+  if (opt.nranks > 1 && opt.variant != SYMM_VARIANT_TILED_ATOMIC && opt.variant != SYMM_VARIANT_AUTO)
+    return set_error(SYMM_ERR_UNSUPPORTED, "multi-rank plans support the tiled_atomic variant only");
   if (opt.vec_width && (opt.vec_width < 1 || opt.vec_width > 32 || (opt.vec_width & (opt.vec_width - 1))))
     return set_error(SYMM_ERR_ARG, "vec_width %d must be a power of two <= 32", opt.vec_width);
   int ndev = 0;
@@ -508,8 +551,13 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   P->vec_order = opt.vec_order;
   P->n = S.n;
   P->nnz = S.nnz;
-  P->row_begin = 0;
-  P->row_end = S.n;
+  std::vector<int32_t> tb, rb, he;
+  partition_tiles(S, opt.nranks, tb, rb, he);
+  P->nranks = opt.nranks;
+  P->rank = opt.rank;
+  P->row_begin = rb[(size_t)opt.rank];
+  P->row_end = rb[(size_t)opt.rank + 1];
+  P->local_end = he[(size_t)opt.rank];
   P->min_bytes = 12 * S.nnz + 4 * ((int64_t)S.n + 1) + 24 * (int64_t)S.n;
   cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, opt.device);
   P->vec = opt.vec_width ? opt.vec_width : pick_vec(S.nnz, S.n);
@@ -519,8 +567,17 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_TILED_ATOMIC || v == SYMM_VARIANT_AUTO;
   bool want_col = all || v == SYMM_VARIANT_COLORED;
   bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
+  if (opt.nranks > 1) {
+    want_col = want_csr = false;
+    P->variant = SYMM_VARIANT_TILED_ATOMIC;
+  }
   if (want_tiled) {
-    rc = build_tiled(P, S);
+    rc = build_tiled(P, S, tb[(size_t)opt.rank], tb[(size_t)opt.rank + 1]);
+    if (rc == SYMM_ERR_UNSUPPORTED && opt.nranks > 1) {
+      free_plan(P);
+      cudaSetDevice(cur);
+      return rc;
+    }
     if (rc == SYMM_ERR_UNSUPPORTED && (v == SYMM_VARIANT_AUTO || all)) {
       rc = SYMM_OK;  // AUTO falls back to the colored variant
       want_col = want_csr = true;
@@ -562,7 +619,12 @@ int symmspmv_plan_rows(const symmspmv_plan_t* p, int32_t* b, int32_t* e) {
 int symmspmv_run_variant(symmspmv_plan_t* P, int32_t variant, const double* x, double* y, void* stream) {
   if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
   if (P->n > 0 && (!x || !y)) return set_error(SYMM_ERR_ARG, "NULL vector");
-  const uintptr_t xa = (uintptr_t)x, ya = (uintptr_t)y, nb = (uintptr_t)P->n * sizeof(double);
+  if (P->nranks > 1 && variant >= 0 && variant != SYMM_VARIANT_TILED_ATOMIC && variant != SYMM_VARIANT_AUTO)
+    return set_error(SYMM_ERR_UNSUPPORTED, "multi-rank plans run the tiled_atomic variant only");
+  if (P->nranks > 1 && P->vec_order != SYMM_ORDER_PERMUTED)
+    return set_error(SYMM_ERR_UNSUPPORTED, "multi-rank plans take x/y in the permuted order");
+  const uintptr_t xa = (uintptr_t)x, ya = (uintptr_t)y,
+                  nb = (uintptr_t)((int64_t)P->local_end - P->row_begin) * sizeof(double);
   if (P->n > 0 && xa < ya + nb && ya < xa + nb) return set_error(SYMM_ERR_ALIAS, "x and y overlap");
   int cur = 0;
   cudaGetDevice(&cur);
@@ -594,6 +656,7 @@ int symmspmv_run(symmspmv_plan_t* P, const double* x, double* y, void* stream) {
 
 int symmspmv_run_host(symmspmv_plan_t* P, const double* x_host, double* y_host, void* stream) {
   if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
+  if (P->nranks > 1) return set_error(SYMM_ERR_UNSUPPORTED, "run_host is single-rank");
   if (P->n == 0) return SYMM_OK;
   if (!x_host || !y_host) return set_error(SYMM_ERR_ARG, "NULL host vector");
   int cur = 0;
@@ -630,6 +693,28 @@ int symmspmv_run_host(symmspmv_plan_t* P, const double* x_host, double* y_host, 
 }
 
 int symmspmv_last_launches(const symmspmv_plan_t* p) { return p ? p->last_launches : 0; }
+
+int symmspmv_plan_local(const symmspmv_plan_t* p, int32_t* b, int32_t* e) {
+  if (!p || !b || !e) return set_error(SYMM_ERR_ARG, "NULL argument");
+  *b = p->row_begin;
+  *e = p->local_end;
+  return SYMM_OK;
+}
+
+int symmspmv_halo_add(double* y, const double* v, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!y || !v))) return set_error(SYMM_ERR_ARG, "bad argument");
+  int rc = launch_add(y, v, n, stream);
+  return rc ? cuda_fail((cudaError_t)rc, "k_add") : SYMM_OK;
+}
+
+int race_schedule_partition(const race_schedule_t* s, int32_t nranks, int32_t* row_bounds, int32_t* halo_end) {
+  if (!s || nranks < 1) return set_error(SYMM_ERR_ARG, "bad argument");
+  std::vector<int32_t> tb, rb, he;
+  partition_tiles(s->S, nranks, tb, rb, he);
+  if (row_bounds) std::copy(rb.begin(), rb.end(), row_bounds);
+  if (halo_end) std::copy(he.begin(), he.end(), halo_end);
+  return SYMM_OK;
+}
 
 int symmspmv_plan_bytes(const symmspmv_plan_t* p, int64_t* device_bytes, int64_t* min_bytes) {
   if (!p) return set_error(SYMM_ERR_ARG, "NULL plan");

@@ -133,5 +133,6 @@ int tiled_smem_bytes(const TiledArgs& T);
 int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);  // returns the ring depth in *out
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 int launch_scatter(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
+int launch_add(double* y, const double* v, int64_t n, void* stream);
 
 }  // namespace symm

@@ -68,6 +68,11 @@ __global__ void k_gather(const double* __restrict__ src, const int32_t* __restri
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) dst[i] = src[idx[i]];
 }
+__global__ void k_add(double* __restrict__ y, const double* __restrict__ v, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) y[i] += v[i];
+}
 __global__ void k_scatter(const double* __restrict__ src, const int32_t* __restrict__ idx, double* __restrict__ dst,
                           int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -423,6 +428,11 @@ int launch_zero(double* y, int64_t n, void* stream) {
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream) {
   if (n <= 0) return 0;
   k_gather<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, idx, dst, n);
+  return (int)cudaGetLastError();
+}
+int launch_add(double* y, const double* v, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  k_add<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(y, v, n);
   return (int)cudaGetLastError();
 }
 int launch_scatter(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream) {

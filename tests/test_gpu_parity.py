@@ -167,3 +167,39 @@ def test_parity_full_size(name):
         y = yd.cpu().numpy()[perm]
         assert relinf(y, y_ref) <= TOL, v
     del plan
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+@pytest.mark.parametrize("name", ["spin_14", "st27_24", "lap3d_40", "fem_knn_30k"])
+def test_multirank_plans_emulated_on_one_gpu(name, ws):
+    """Per-rank plans (own tiles only, shifted local vectors) run one after the
+    other on one GPU; the halo exchange is emulated by copies.  Kernels never
+    wait on each other (B200_PROFILING.md: no co-scheduled waiting ranks)."""
+    torch = _torch()
+    import paper_1907_06487_b200 as P
+    from paper_1907_06487_b200.dist import halo_pieces
+
+    U, x = gen.make_config(name)
+    y_ref = oracle.symmspmv(U, x)
+    s = P.build_schedule(U)
+    perm, inv = s.permutation()
+    xp = x[inv]
+    b, h = s.partition(ws)
+    yl = []
+    for r in range(ws):
+        plan = P.Plan(s, U, variant="tiled_atomic", nranks=ws, rank=r)
+        r0, he = plan.local_range()
+        assert (r0, he) == (int(b[r]), int(h[r]))
+        xd = torch.from_numpy(xp[r0:he].copy()).cuda()
+        yd = torch.full_like(xd, float("nan"))
+        plan.run(xd, yd)
+        torch.cuda.synchronize()
+        yl.append(yd.cpu().numpy())
+    y = np.empty(U.n)
+    for r in range(ws):
+        r0, r1 = int(b[r]), int(b[r + 1])
+        y[r0:r1] = yl[r][:r1 - r0]
+    for p in range(ws):
+        for (q, a, c) in halo_pieces(b, h, p):
+            y[a:c] += yl[p][a - b[p]:c - b[p]]
+    assert relinf(y[perm], y_ref) <= TOL
