@@ -242,6 +242,24 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
     dist.all_gather(gathered, pad)
     hb = torch.tensor([D.hx.halo_bytes()], device="cuda")
     dist.all_reduce(hb, op=dist.ReduceOp.MAX)
+    # e2e: every step copies this rank's x slice in from pinned host memory and
+    # its y rows back out (device-timed, max over ranks)
+    xh = torch.from_numpy(xp[r0:r1].copy()).pin_memory()
+    yh = torch.empty(D.n_own, dtype=torch.float64).pin_memory()
+    xe, ye = D.empty_local(), D.empty_local()
+    e2e_steps = max(5, min(50, a.steps // 20))
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record(stream)
+    for _ in range(e2e_steps):
+        xe[:D.n_own].copy_(xh, non_blocking=True)
+        D.run(xe, ye)
+        yh.copy_(ye[:D.n_own], non_blocking=True)
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([ev2.elapsed_time(ev3) / e2e_steps], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
     if rank == 0:
         yperm = np.concatenate([gathered[r][:int(all_sizes[r].item())].cpu().numpy() for r in range(ws)])
         y = yperm[perm]
@@ -261,7 +279,8 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
                          "frac": achieved / (peak * ws), "traffic": None, "bytes_per_launch": bytes_min,
                          "peak_source": peak_src + f" x {ws} GPUs"},
             "cpu_baseline": None,
-            "e2e": None,
+            "e2e": {"value": 2.0 * nf / (float(te.item()) / 1e3) / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n, "ms_per_step": float(te.item())},
             "clocks": clk.report(),
             "schedule": {"build_s": t_sched, "plan_s": t_plan, "gen_s": t_gen},
             "y_checksum": float(np.sum(np.abs(y))),

@@ -405,6 +405,13 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     if (cfg.reorder) {
       for (int32_t v = 0; v < n; ++v) S->level_ptr[(size_t)S->dist[(size_t)v] + 1] += 1;
       for (int32_t l = 0; l < totalLvl; ++l) S->level_ptr[(size_t)l + 1] += S->level_ptr[(size_t)l];
+      if (cfg.flags & 1u) {
+        // within-level order = original index (instead of BFS discovery order);
+        // levels stay contiguous and in BFS order
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int32_t l = 0; l < totalLvl; ++l)
+          std::sort(order.begin() + S->level_ptr[(size_t)l], order.begin() + S->level_ptr[(size_t)l + 1]);
+      }
     } else {
       // no reordering: the whole matrix is one "level" (natural order kept)
       S->level_ptr = {0, n};
