@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--tile-window", type=int, default=0, help="race_config.max_tile_window override")
     ap.add_argument("--tile-work", type=int, default=0, help="race_config.tile_work override")
     ap.add_argument("--vec", type=int, default=0, help="lanes per row override")
+    ap.add_argument("--sched", action="append", default=[], help="race_config override key=value (repeatable)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-rank path (row blocks + halo) even with one rank (tests the glue)")
     return ap.parse_args()
@@ -325,6 +326,9 @@ def main():
         sched_kw["max_tile_rows"] = a.tile_window
     if a.tile_work:
         sched_kw["tile_work"] = a.tile_work
+    for kv in a.sched:
+        k_, v_ = kv.split("=")
+        sched_kw[k_] = int(v_)
     s = P.build_schedule(U, **sched_kw)
     t_sched = time.perf_counter() - t0
     st = s.stats

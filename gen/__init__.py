@@ -214,8 +214,15 @@ SMALL_CONFIGS = {
 }
 
 
+# Mid-size members used for profiling and scaling studies (not BASELINE configs).
+EXTRA_CONFIGS = {
+    "lap3d_256": dict(build=lambda: lap3d(256, 5, True), x_seed=105),
+    "fem_knn_1M": dict(build=lambda: knn(1_000_000, 20, 3), x_seed=103),
+}
+
+
 def make_config(name: str):
-    spec = CONFIGS.get(name) or SMALL_CONFIGS[name]
+    spec = CONFIGS.get(name) or SMALL_CONFIGS.get(name) or EXTRA_CONFIGS[name]
     U = spec["build"]()
     U.name = name
     return U, vector_uniform(U.n, spec["x_seed"])

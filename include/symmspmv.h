@@ -77,8 +77,12 @@ typedef struct {
   int32_t max_tile_window;  /* cap on |own rows ∪ targets| per tile (smem entries)           */
   int32_t max_tile_nnz;     /* cap on stored entries per tile (smem staging of the tile)     */
   int32_t reorder;          /* 1 = BFS level permutation; 0 = keep order */
+  int32_t cone_tiles;       /* 0 = contiguous tiles (default); 1/2 = tiles are cones across the
+                               levels of their level group (1: proportional cuts, 2: cuts
+                               follow BFS discovery), rows re-permuted inside the group */
+  int32_t min_group_levels; /* >= k: minimum levels per level group ("at least k") */
   int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
-  uint32_t flags;           /* reserved, 0                                                   */
+  uint32_t flags;           /* bit 0: within-level order = original index (experimental)    */
 } race_config;
 
 typedef struct race_schedule race_schedule_t;

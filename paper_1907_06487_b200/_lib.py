@@ -25,7 +25,8 @@ class SymmCsrUpper(C.Structure):
 class RaceConfig(C.Structure):
     _fields_ = [("k", C.c_int32), ("n_workers", C.c_int32), ("tile_work", C.c_int32), ("balance_by", C.c_int32),
                 ("root", C.c_int32), ("n_eps", C.c_int32), ("eps", C.c_double * 8), ("max_tile_rows", C.c_int32),
-                ("max_tile_window", C.c_int32), ("max_tile_nnz", C.c_int32), ("reorder", C.c_int32), ("validate", C.c_int32),
+                ("max_tile_window", C.c_int32), ("max_tile_nnz", C.c_int32), ("reorder", C.c_int32), ("cone_tiles", C.c_int32),
+                ("min_group_levels", C.c_int32), ("validate", C.c_int32),
                 ("flags", C.c_uint32)]
 
 

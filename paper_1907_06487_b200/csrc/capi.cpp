@@ -404,6 +404,8 @@ void race_config_default(race_config* c) {
   c->max_tile_window = 768;
   c->max_tile_nnz = 1536;
   c->reorder = 1;
+  c->cone_tiles = 0;
+  c->min_group_levels = 2;
   c->validate = 1;
   c->flags = 0;
 }

@@ -360,6 +360,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   S->n = n;
   S->nnz = U->nnz;
   const int k = cfg.k;
+  const int kg = std::max(k, cfg.min_group_levels);  // levels per group: "at least k"
 
   // ---- a2 mirror, a3 roots, a4 BFS levels (discovery order) -------------------
   std::vector<int64_t> gp;
@@ -368,6 +369,10 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   S->dist.assign((size_t)n, -1);
   std::vector<int32_t> order;
   order.reserve((size_t)n);
+  // disc[p]: BFS position of the first vertex discovered by the vertex at BFS
+  // position p (= queue length when p is expanded); the children first
+  // discovered by positions [a, b) of one level are positions [disc[a], disc[b])
+  std::vector<int32_t> disc((size_t)n + 1, n);
   {
     BfsScratch B;
     B.mark.assign((size_t)n, 0);
@@ -390,6 +395,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
         maxLvl = std::max(maxLvl, lvl);
         for (size_t q = lvl_begin; q < lvl_end; ++q) {
           int32_t u = order[q];
+          disc[q] = (int32_t)order.size();
           for (int64_t e = gp[(size_t)u]; e < gp[(size_t)u + 1]; ++e) {
             int32_t j = ga[(size_t)e];
             if (S->dist[(size_t)j] == -1) { S->dist[(size_t)j] = lvl + 1; order.push_back(j); }
@@ -419,13 +425,12 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
       std::iota(order.begin(), order.end(), 0);
     }
   }
-  { std::vector<int64_t>().swap(gp); std::vector<int32_t>().swap(ga); }
 
   // ---- a5 permutation and U' = upper(P A P^T) ---------------------------------
   S->inv = order;
   S->perm.assign((size_t)n, 0);
   for (int32_t i = 0; i < n; ++i) S->perm[(size_t)order[(size_t)i]] = i;
-  {
+  auto build_permuted = [&]() {
     const int32_t* P = S->perm.data();
     std::vector<int32_t> cnt((size_t)n + 1, 0);
     int64_t bwb = 0;
@@ -471,8 +476,9 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     }
     }
     S->bw_after = bwa;
-  }
-  const int32_t* rp = S->prow_ptr.data();
+  };
+  build_permuted();
+  const int32_t* rp = S->prow_ptr.data();  // re-bound after the cone re-permutation
   const int32_t* pc = S->pcol.data();
 
   // ---- a6 eps aggregation (§4.4.3) + Alg. 4 (§4.3), work per level ------------
@@ -489,27 +495,181 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     total_work += w;
   }
   int64_t nworkers = cfg.n_workers > 0 ? cfg.n_workers : std::max<int64_t>(1, (total_work + cfg.tile_work - 1) / cfg.tile_work);
-  S->windows = eps_aggregate(lw, nworkers, k, cfg.eps[0]);
+  S->windows = eps_aggregate(lw, nworkers, kg, cfg.eps[0]);
   {
     std::vector<int32_t> T, wk;
     const size_t nw = S->windows.size() / 3;
     if (nw > 0) T.push_back(S->windows[0]);
     for (size_t w = 0; w < nw; ++w) {
       int32_t f = S->windows[3 * w], e = S->windows[3 * w + 1], b = S->windows[3 * w + 2];
-      int32_t m = split_window(lw, f, e, k);
+      int32_t m = split_window(lw, f, e, kg);
       T.push_back(m);
       T.push_back(e);
       wk.push_back(b);
       wk.push_back(b);
     }
-    if (T.size() >= 3) alg4_balance(T, wk, lw, k);
+    if (T.size() >= 3) alg4_balance(T, wk, lw, kg);
     S->group_lvl = T;
     S->group_workers = wk;
   }
   const int32_t ngroups = (int32_t)S->group_workers.size();
 
-  // ---- a7 tiles: split every group into `workers` contiguous work-balanced chunks,
-  //      then enforce the row / smem-window caps by halving ----------------------
+  // ---- a7 tiles --------------------------------------------------------------
+  // (a) cone tiles (cfg.cone_tiles, reading R26): inside level group g with b_g
+  //     workers, every level of the group is cut into K work-balanced chunks and
+  //     tile k = chunk k of every level; the rows of the group are re-permuted
+  //     cone by cone (levels stay contiguous per group).  K
+  //     starts at b_g and grows until every cone meets the row / nnz / window
+  //     caps in the FINAL order.
+  // (b) otherwise (or if no K fits): contiguous work-balanced chunks of the
+  //     group, halved until they fit.
+  std::vector<std::vector<int32_t>> cone_sizes((size_t)ngroups);
+  std::vector<char> is_cone((size_t)ngroups, 0);
+  if (cfg.cone_tiles && cfg.reorder && ngroups > 0 && n > 0) {
+    std::vector<uint8_t> has_diag((size_t)n, 0);
+    for (int32_t r = 0; r < n; ++r)
+      has_diag[(size_t)r] = (U->row_ptr[r] < U->row_ptr[r + 1] && U->col[U->row_ptr[r]] == r);
+    std::vector<int32_t> grp_of_lvl((size_t)totalLvl, 0);
+    for (int32_t g = 0; g < ngroups; ++g)
+      for (int32_t l = S->group_lvl[(size_t)g]; l < S->group_lvl[(size_t)g + 1]; ++l) grp_of_lvl[(size_t)l] = g;
+    std::vector<std::vector<int32_t>> new_order((size_t)ngroups);
+    const int32_t* Pb = S->perm.data();  // old -> BFS position
+    const int32_t* Ib = S->inv.data();   // BFS position -> old
+#pragma omp parallel
+    {
+      std::vector<int32_t> cone_of, tg;
+#pragma omp for schedule(dynamic, 1)
+      for (int32_t g = 0; g < ngroups; ++g) {
+        const int32_t l0 = S->group_lvl[(size_t)g], l1 = S->group_lvl[(size_t)g + 1];
+        const int32_t g0 = S->level_ptr[(size_t)l0], g1 = S->level_ptr[(size_t)l1];
+        if (g1 <= g0) continue;
+        int64_t stored = 0;
+        for (int32_t r = g0; r < g1; ++r) stored += rp[r + 1] - rp[r];
+        int64_t K = std::max<int64_t>({(int64_t)S->group_workers[(size_t)g],
+                                       (int64_t)std::ceil((double)stored / (0.9 * cfg.max_tile_nnz)),
+                                       (int64_t)std::ceil((double)(g1 - g0) / cfg.max_tile_rows), 1});
+        cone_of.assign((size_t)(g1 - g0), 0);
+        bool ok = false;
+        std::vector<std::vector<int32_t>> cuts;
+        for (int attempt = 0; attempt < 40 && !ok; ++attempt) {
+          cuts.assign((size_t)(l1 - l0), {});
+          if (cfg.cone_tiles == 2) {
+            // first level: work-balanced cuts; deeper levels: the discovery
+            // ranges of the previous level's chunks (children follow parents)
+            const int32_t a = S->level_ptr[(size_t)l0], e = S->level_ptr[(size_t)l0 + 1];
+            int64_t lwk = 0;
+            for (int32_t r = a; r < e; ++r) lwk += row_work(r);
+            auto& c0 = cuts[0];
+            c0.assign((size_t)K + 1, e);
+            c0[0] = a;
+            int64_t cum = 0, j = 1;
+            for (int32_t r = a; r < e && j < K; ++r) {
+              cum += row_work(r);
+              while (j < K && cum * K >= j * lwk) c0[(size_t)j++] = r + 1;
+            }
+            for (int32_t l = l0 + 1; l < l1; ++l) {
+              const auto& cp = cuts[(size_t)(l - 1 - l0)];
+              auto& c = cuts[(size_t)(l - l0)];
+              const int32_t la = S->level_ptr[(size_t)l], le = S->level_ptr[(size_t)l + 1];
+              c.assign((size_t)K + 1, le);
+              c[0] = la;
+              for (int64_t q = 1; q < K; ++q) {
+                const int32_t pq = cp[(size_t)q];
+                int32_t v = (pq < S->level_ptr[(size_t)l]) ? disc[(size_t)pq] : le;
+                c[(size_t)q] = std::min(std::max(v, c[(size_t)q - 1]), le);
+              }
+            }
+            for (int32_t l = l0; l < l1; ++l) {
+              const auto& c = cuts[(size_t)(l - l0)];
+              for (int64_t q = 0; q < K; ++q)
+                for (int32_t r = c[(size_t)q]; r < c[(size_t)q + 1]; ++r) cone_of[(size_t)(r - g0)] = (int32_t)q;
+            }
+          } else
+          for (int32_t l = l0; l < l1; ++l) {
+            const int32_t a = S->level_ptr[(size_t)l], e = S->level_ptr[(size_t)l + 1];
+            int64_t lwk = 0;
+            for (int32_t r = a; r < e; ++r) lwk += row_work(r);
+            auto& c = cuts[(size_t)(l - l0)];
+            c.assign((size_t)K + 1, e);
+            c[0] = a;
+            int64_t cum = 0;
+            int64_t j = 1;
+            for (int32_t r = a; r < e && j < K; ++r) {
+              cum += row_work(r);
+              while (j < K && cum * K >= j * lwk) c[(size_t)j++] = r + 1;
+            }
+            for (int64_t q = 0; q < K; ++q)
+              for (int32_t r = c[(size_t)q]; r < c[(size_t)q + 1]; ++r) cone_of[(size_t)(r - g0)] = (int32_t)q;
+          }
+          // exact caps of every cone in the final order: entry (r, v) is stored in
+          // row r iff key(v) > key(r), key = (group, cone, BFS position)
+          std::vector<int64_t> rows((size_t)K, 0), nnzc((size_t)K, 0);
+          std::vector<std::vector<int32_t>> tgts((size_t)K);
+          for (int32_t r = g0; r < g1; ++r) {
+            const int32_t kr = cone_of[(size_t)(r - g0)];
+            rows[(size_t)kr]++;
+            const int32_t o = Ib[r];
+            nnzc[(size_t)kr] += has_diag[(size_t)o];
+            for (int64_t e = gp[(size_t)o]; e < gp[(size_t)o + 1]; ++e) {
+              const int32_t v = Pb[ga[(size_t)e]];
+              bool later, same_cone = false;
+              if (v >= g1) later = true;
+              else if (v < g0) later = false;
+              else {
+                const int32_t kv = cone_of[(size_t)(v - g0)];
+                same_cone = (kv == kr);
+                later = kv > kr || (same_cone && v > r);
+              }
+              if (!later) continue;
+              nnzc[(size_t)kr]++;
+              if (!same_cone) tgts[(size_t)kr].push_back(v);
+            }
+          }
+          ok = true;
+          for (int64_t q = 0; q < K && ok; ++q) {
+            auto& t = tgts[(size_t)q];
+            std::sort(t.begin(), t.end());
+            const int64_t w = rows[(size_t)q] + (int64_t)(std::unique(t.begin(), t.end()) - t.begin());
+            if (rows[(size_t)q] > cfg.max_tile_rows || nnzc[(size_t)q] > cfg.max_tile_nnz || w > cfg.max_tile_window)
+              ok = false;
+          }
+          if (!ok) {
+            int64_t maxlvl = 0;
+            for (int32_t l = l0; l < l1; ++l) maxlvl = std::max<int64_t>(maxlvl, S->level_ptr[(size_t)l + 1] - S->level_ptr[(size_t)l]);
+            if (K >= maxlvl) break;  // cannot cut finer: fall back to contiguous chunks
+            K = std::min<int64_t>(maxlvl, K + std::max<int64_t>(1, K / 5));
+          }
+        }
+        if (!ok) continue;
+        is_cone[(size_t)g] = 1;
+        auto& ord = new_order[(size_t)g];
+        ord.reserve((size_t)(g1 - g0));
+        for (int64_t q = 0; q < K; ++q) {
+          const size_t before = ord.size();
+          for (int32_t l = l0; l < l1; ++l) {
+            const auto& c = cuts[(size_t)(l - l0)];
+            for (int32_t r = c[(size_t)q]; r < c[(size_t)q + 1]; ++r) ord.push_back(r);
+          }
+          if (ord.size() > before) cone_sizes[(size_t)g].push_back((int32_t)(ord.size() - before));
+        }
+      }
+    }
+    // final order: cone groups re-permuted, other groups unchanged
+    std::vector<int32_t> fin((size_t)n);  // final position -> BFS position
+    for (int32_t g = 0; g < ngroups; ++g) {
+      const int32_t g0 = S->level_ptr[(size_t)S->group_lvl[(size_t)g]], g1 = S->level_ptr[(size_t)S->group_lvl[(size_t)g + 1]];
+      if (is_cone[(size_t)g]) std::copy(new_order[(size_t)g].begin(), new_order[(size_t)g].end(), fin.begin() + g0);
+      else for (int32_t r = g0; r < g1; ++r) fin[(size_t)r] = r;
+    }
+    std::vector<int32_t> inv2((size_t)n);
+    for (int32_t f = 0; f < n; ++f) inv2[(size_t)f] = S->inv[(size_t)fin[(size_t)f]];
+    S->inv.swap(inv2);
+    for (int32_t f = 0; f < n; ++f) S->perm[(size_t)S->inv[(size_t)f]] = f;
+    build_permuted();
+    rp = S->prow_ptr.data();
+    pc = S->pcol.data();
+  }
+  { std::vector<int64_t>().swap(gp); std::vector<int32_t>().swap(ga); }
   auto window_of = [&](int32_t r0, int32_t r1) -> int64_t {
     std::vector<int32_t> t;
     for (int32_t r = r0; r < r1; ++r)
@@ -525,6 +685,14 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
       int32_t r0 = S->level_ptr[(size_t)S->group_lvl[(size_t)g]];
       int32_t r1 = S->level_ptr[(size_t)S->group_lvl[(size_t)g + 1]];
       if (r1 <= r0) continue;
+      if (is_cone[(size_t)g]) {
+        int32_t a = r0;
+        for (int32_t sz : cone_sizes[(size_t)g]) {
+          per_group[(size_t)g].push_back({a, a + sz});
+          a += sz;
+        }
+        continue;
+      }
       int64_t gw = 0;
       for (int32_t r = r0; r < r1; ++r) gw += row_work(r);
       int64_t b = std::max<int64_t>(1, S->group_workers[(size_t)g]);
