@@ -7,7 +7,6 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
-#include <numeric>
 #include <string>
 #include <vector>
 
@@ -149,150 +148,52 @@ void partition_tiles(const Schedule& S, int nranks, std::vector<int32_t>& tile_b
 int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t t_end) {
   const int32_t nt = (int32_t)S.tile_group.size();
   const int32_t n = S.n;
+  std::vector<int32_t> tile_of((size_t)n);
+  for (int32_t t = 0; t < nt; ++t)
+    for (int32_t r = S.tile_ptr[(size_t)t]; r < S.tile_ptr[(size_t)t + 1]; ++r) tile_of[(size_t)r] = t;
   std::vector<TileDesc> desc((size_t)nt);
-  std::vector<std::vector<unsigned char>> tblk((size_t)nt);
-  int bad = 0, badmiss = 0;
-  // per tile: SELL-32 row slices + CSC slices (see TileDesc in internal.h)
-#pragma omp parallel for schedule(dynamic, 8) reduction(max : bad) reduction(| : badmiss)
+  std::vector<int64_t> boff((size_t)nt + 1, 0);
+  int32_t block_cap = 16, window_cap = 2, nnz_cap = 2;
+  int bad = 0;
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
-    const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
-    const int32_t ns = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
-    const int32_t W = T + ns;
-    const int32_t e0 = S.prow_ptr[(size_t)r0];
-    const int32_t nnz = S.prow_ptr[(size_t)r1] - e0;
-    std::vector<int32_t> lc((size_t)nnz), er((size_t)nnz);  // local column / local row of entry
-    std::vector<int32_t> rl((size_t)T), cl((size_t)W, 0);
-    for (int32_t r = r0; r < r1; ++r) {
-      rl[(size_t)(r - r0)] = S.prow_ptr[(size_t)r + 1] - S.prow_ptr[(size_t)r];
-      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
-        const int32_t c = S.pcol[(size_t)i];
-        int32_t l;
-        if (c < r1) l = c - r0;
-        else {
-          const int32_t* it = std::lower_bound(sp, sp + ns, c, [](int32_t a, int32_t v) {
-            return (int32_t)((uint32_t)a & kIdxMask) < v;
-          });
-          if (it == sp + ns || (int32_t)((uint32_t)*it & kIdxMask) != c) badmiss |= 1;
-          l = T + (int32_t)(it - sp);
-        }
-        lc[(size_t)(i - e0)] = l;
-        er[(size_t)(i - e0)] = r - r0;
-        if (c != r) cl[(size_t)l]++;
-      }
-    }
-    // own rows longest first; targets: own rows (that order), then spill targets longest first
-    std::vector<int32_t> ro((size_t)T), so((size_t)ns);
-    std::iota(ro.begin(), ro.end(), 0);
-    std::stable_sort(ro.begin(), ro.end(), [&](int32_t a, int32_t b) { return rl[(size_t)a] > rl[(size_t)b]; });
-    std::iota(so.begin(), so.end(), T);
-    std::stable_sort(so.begin(), so.end(), [&](int32_t a, int32_t b) { return cl[(size_t)a] > cl[(size_t)b]; });
-    const int32_t R = (T + 31) / 32, Cn = (W + 31) / 32;
-    std::vector<int32_t> tt((size_t)Cn * 32, 0xffff);
-    for (int32_t q = 0; q < T; ++q) tt[(size_t)q] = ro[(size_t)q];
-    for (int32_t q = 0; q < ns; ++q) tt[(size_t)(T + q)] = so[(size_t)q];
-    std::vector<int32_t> rofs((size_t)R + 1, 0), cofs((size_t)Cn + 1, 0), rlen((size_t)R * 32, 0), clen((size_t)Cn * 32, 0);
-    for (int32_t sI = 0; sI < R; ++sI) {
-      int32_t w = 0;
-      for (int32_t j = 0; j < 32; ++j) {
-        const int32_t q = sI * 32 + j;
-        if (q < T) { rlen[(size_t)q] = rl[(size_t)ro[(size_t)q]]; w = std::max(w, rlen[(size_t)q]); }
-      }
-      rofs[(size_t)sI + 1] = rofs[(size_t)sI] + 32 * w;
-    }
-    for (int32_t sI = 0; sI < Cn; ++sI) {
-      int32_t w = 0;
-      for (int32_t j = 0; j < 32; ++j) {
-        const int32_t q = sI * 32 + j;
-        if (tt[(size_t)q] != 0xffff) { clen[(size_t)q] = cl[(size_t)tt[(size_t)q]]; w = std::max(w, clen[(size_t)q]); }
-      }
-      cofs[(size_t)sI + 1] = cofs[(size_t)sI] + 32 * w;
-    }
-    const int32_t nr_flat = rofs[(size_t)R], nc_flat = cofs[(size_t)Cn];
-    // block offsets
-    const int64_t o_tt = (int64_t)sizeof(TileDesc);
-    const int64_t o_rofs = align16(o_tt + 2 * 32 * (int64_t)Cn);
-    const int64_t o_rlen = align16(o_rofs + 2 * (int64_t)(R + 1));
-    const int64_t o_cofs = align16(o_rlen + 2 * 32 * (int64_t)R);
-    const int64_t o_clen = align16(o_cofs + 2 * (int64_t)(Cn + 1));
-    const int64_t o_tc = align16(o_clen + 2 * 32 * (int64_t)Cn);
-    const int64_t o_lcol = align16(o_tc + 4 * (int64_t)nc_flat);
-    const int64_t o_tgt = align16(o_lcol + 2 * (int64_t)nr_flat);
-    const int64_t o_val = align16(o_tgt + 4 * (int64_t)ns);
-    const int64_t bytes = align16(o_val + 8 * (int64_t)nr_flat);
-    if (nr_flat >= 65536 || W >= 65535 || bytes >= 65536) { bad = std::max(bad, t + 1); continue; }
+    const int32_t S_ = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
+    const int64_t nnz = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
+    int32_t nd = 0;
+    for (int32_t r = r0; r < r1; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
+    const int64_t W = (int64_t)T + S_;
+    const int64_t o_start = (int64_t)sizeof(TileDesc);
+    int64_t o_lcol = align16(o_start + 2 * (int64_t)(T + 1));
+    int64_t o_tidx = align16(o_lcol + 2 * nnz);
+    int64_t o_tptr = align16(o_tidx + 4 * (nnz - nd));
+    int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
+    int64_t o_slot = o_tgt;
+    int64_t o_val = align16(o_tgt + 4 * (int64_t)S_);
+    int64_t bytes = align16(o_val + 8 * nnz);
+    if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
     TileDesc& D = desc[(size_t)t];
     std::memset(&D, 0, sizeof D);
     D.block_bytes = (int32_t)bytes;
     D.nrows = T;
-    D.nspill = ns;
-    D.nnz = nnz;
+    D.nspill = S_;
+    D.nnz = (int32_t)nnz;
     D.row0 = r0;
-    D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
-    D.o_ro = 0;
-    D.o_tt = (uint16_t)o_tt;
-    D.o_rofs = (uint16_t)o_rofs;
-    D.o_rlen = (uint16_t)o_rlen;
-    D.o_cofs = (uint16_t)o_cofs;
-    D.o_clen = (uint16_t)o_clen;
-    D.o_tc = (uint16_t)o_tc;
     D.o_lcol = (uint16_t)o_lcol;
+    D.o_tidx = (uint16_t)o_tidx;
+    D.o_tptr = (uint16_t)o_tptr;
     D.o_tgt = (uint16_t)o_tgt;
+    D.o_slot = (uint16_t)o_slot;
     D.o_val = (uint16_t)o_val;
-    D.nrs = (uint16_t)R;
-    D.ncs = (uint16_t)Cn;
-    auto& blk = tblk[(size_t)t];
-    blk.assign((size_t)bytes, 0);
-    uint16_t* ptt = reinterpret_cast<uint16_t*>(blk.data() + o_tt);
-    uint16_t* profs = reinterpret_cast<uint16_t*>(blk.data() + o_rofs);
-    uint16_t* prlen = reinterpret_cast<uint16_t*>(blk.data() + o_rlen);
-    uint16_t* pcofs = reinterpret_cast<uint16_t*>(blk.data() + o_cofs);
-    uint16_t* pclen = reinterpret_cast<uint16_t*>(blk.data() + o_clen);
-    uint32_t* ptc = reinterpret_cast<uint32_t*>(blk.data() + o_tc);
-    uint16_t* plcol = reinterpret_cast<uint16_t*>(blk.data() + o_lcol);
-    int32_t* ptgt = reinterpret_cast<int32_t*>(blk.data() + o_tgt);
-    double* pval = reinterpret_cast<double*>(blk.data() + o_val);
-    for (int32_t q = 0; q < Cn * 32; ++q) { ptt[q] = (uint16_t)tt[(size_t)q]; pclen[q] = (uint16_t)clen[(size_t)q]; }
-    for (int32_t q = 0; q <= R; ++q) profs[q] = (uint16_t)rofs[(size_t)q];
-    for (int32_t q = 0; q < R * 32; ++q) prlen[q] = (uint16_t)rlen[(size_t)q];
-    for (int32_t q = 0; q <= Cn; ++q) pcofs[q] = (uint16_t)cofs[(size_t)q];
-    for (int32_t j = 0; j < ns; ++j) ptgt[j] = (int32_t)((uint32_t)sp[j] & kIdxMask);
-    // row part: entry i of own row ro[q] (q = 32 s + j) at rofs[s] + 32 i + j; remember flat index
-    std::vector<int32_t> flat((size_t)nnz);
-    for (int32_t q = 0; q < T; ++q) {
-      const int32_t lr = ro[(size_t)q], sI = q / 32, j = q % 32;
-      const int32_t eb = S.prow_ptr[(size_t)(r0 + lr)] - e0;
-      for (int32_t i = 0; i < rl[(size_t)lr]; ++i) {
-        const int32_t f = rofs[(size_t)sI] + 32 * i + j;
-        flat[(size_t)(eb + i)] = f;
-        plcol[f] = (uint16_t)lc[(size_t)(eb + i)];
-        pval[f] = S.pval[(size_t)(e0 + eb + i)];
-      }
-    }
-    // CSC part: transposed entries of target tt[q] in stored entry order
-    std::vector<int32_t> pos_of((size_t)W, -1), fill((size_t)W, 0);
-    for (int32_t q = 0; q < Cn * 32; ++q)
-      if (tt[(size_t)q] != 0xffff) pos_of[(size_t)tt[(size_t)q]] = q;
-    for (int32_t e = 0; e < nnz; ++e) {
-      const int32_t l = lc[(size_t)e];
-      if (l == er[(size_t)e]) continue;  // diagonal
-      const int32_t q = pos_of[(size_t)l], sI = q / 32, j = q % 32;
-      const int32_t f = cofs[(size_t)sI] + 32 * fill[(size_t)l]++ + j;
-      ptc[f] = (uint32_t)flat[(size_t)e] | ((uint32_t)er[(size_t)e] << 16);
-    }
+    D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
+    boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
+    D.block_off = boff[(size_t)t];
+    block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
+    window_cap = std::max<int32_t>(window_cap, (int32_t)W);
+    nnz_cap = std::max<int32_t>(nnz_cap, (int32_t)nnz);
   }
   if (bad)
     return set_error(SYMM_ERR_UNSUPPORTED, "tile %d does not fit the 64 KB tile-block format (use smaller tiles)", bad - 1);
-  std::vector<int64_t> boff((size_t)nt + 1, 0);
-  int32_t block_cap = 16, window_cap = 2, nnz_cap = 2;
-  for (int32_t t = 0; t < nt; ++t) {
-    TileDesc& D = desc[(size_t)t];
-    boff[(size_t)t + 1] = boff[(size_t)t] + D.block_bytes;
-    D.block_off = boff[(size_t)t];
-    block_cap = std::max<int32_t>(block_cap, D.block_bytes);
-    window_cap = std::max<int32_t>(window_cap, D.nrows + D.nspill);
-    nnz_cap = std::max<int32_t>(nnz_cap, D.nnz);
-  }
   window_cap = (window_cap + 2 + 15) & ~15;  // +2: x window alignment shift; stages stay 128-B aligned
   block_cap = (block_cap + 127) & ~127;
   // staged contributions: slot order = (owner row, writer tile, ...) -> contiguous per row
@@ -306,13 +207,50 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
       slots[(size_t)q] = pos[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)]++;
   }
   std::vector<unsigned char> blocks((size_t)boff[(size_t)nt], 0);
-#pragma omp parallel for schedule(dynamic, 64)
+#pragma omp parallel for schedule(dynamic, 8) reduction(| : bad)
   for (int32_t t = 0; t < nt; ++t) {
-    std::memcpy(blocks.data() + boff[(size_t)t], tblk[(size_t)t].data(), tblk[(size_t)t].size());
-    std::memcpy(blocks.data() + boff[(size_t)t], &desc[(size_t)t], sizeof(TileDesc));  // descriptor travels with its block
-    std::vector<unsigned char>().swap(tblk[(size_t)t]);
+    const TileDesc& D = desc[(size_t)t];
+    const int32_t r0 = D.row0, T = D.nrows, r1 = r0 + T, ns = D.nspill, W = T + ns;
+    const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
+    unsigned char* blk = blocks.data() + D.block_off;
+    std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
+    uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
+    uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
+    uint32_t* tcsc = reinterpret_cast<uint32_t*>(blk + D.o_tidx);
+    uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
+    int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
+    double* val = reinterpret_cast<double*>(blk + D.o_val);
+    for (int32_t j = 0; j < ns; ++j) tgt[j] = (int32_t)((uint32_t)sp[j] & kIdxMask);
+    const int32_t e0 = S.prow_ptr[(size_t)r0];
+    std::vector<int32_t> tcnt((size_t)W + 1, 0);
+    for (int32_t r = r0; r < r1; ++r) {
+      start[r - r0] = (uint16_t)(S.prow_ptr[(size_t)r] - e0);
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+        const int32_t c = S.pcol[(size_t)i];
+        int32_t l;
+        if (c < r1) l = c - r0;
+        else {
+          int32_t lo = 0, hi = ns;
+          while (lo < hi) {
+            int32_t mid = (lo + hi) / 2;
+            if (tgt[mid] < c) lo = mid + 1;
+            else hi = mid;
+          }
+          if (lo >= ns || tgt[lo] != c) bad |= 1;
+          l = T + lo;
+        }
+        lcol[i - e0] = (uint16_t)l;
+        val[i - e0] = S.pval[(size_t)i];
+        if (c != r) tcnt[(size_t)l + 1]++;
+      }
+    }
+    start[T] = (uint16_t)(S.prow_ptr[(size_t)r1] - e0);
+    for (int32_t l = 0; l < W; ++l) tcnt[(size_t)l + 1] += tcnt[(size_t)l];
+    for (int32_t l = 0; l <= W; ++l) tptr[l] = (uint16_t)tcnt[(size_t)l];
+    for (int32_t r = r0; r < r1; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
+        if (S.pcol[(size_t)i] != r) tcsc[tcnt[lcol[i - e0]]++] = (uint32_t)(i - e0) | ((uint32_t)(r - r0) << 16);
   }
-  bad = badmiss;
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   // multi-rank: keep only this rank's tiles (descriptors re-based to the range)
   if (t_begin != 0 || t_end != nt) {

@@ -67,33 +67,24 @@ constexpr uint32_t kFirstBit = 0x80000000u;
 constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
-// The tile's block (one cp.async.bulk into shared memory), 16-B aligned parts:
-//   TileDesc (64 B)
-//   ro   u16[T]        : own rows in processing order (longest row first)
-//   tt   u16[32*C]     : local target of lane j of slice s (own rows first, in
-//                        `ro` order, then spill targets); 0xffff = idle lane
-//   rofs u16[R+1]      : start (in entries) of row slice s, R = ceil(T/32)
-//   rlen u16[32*R]     : stored entries of the row of lane j of row slice s
-//   cofs u16[C+1]      : start (in entries) of CSC slice s, C = ceil(W/32)
-//   clen u16[32*C]     : transposed entries of the target of lane j of slice s
-//   tc   u32[cofs[C]]  : CSC entries, (index into val|lcol << 0) | (local row << 16)
-//   lcol u16[rofs[R]]  : local column of every stored entry (row slices)
-//   tgt  i32[S]        : global row of each spill target
-//   val  f64[rofs[R]]  : values (row slices)
-// Slices are SELL-32: entry i of lane j of slice s sits at ofs[s] + 32*i + j,
-// so a warp reads 32 consecutive words per step (no bank conflicts).  Local
-// ids: own rows 0..T-1 (natural order), spill targets T..W-1.
+// The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
+//   TileDesc (64 B) | start u16[T+1] | lcol u16[nnz] | tcsc u32[noff] |
+//   tptr u16[W+1] | tgt i32[S] | val f64[nnz]
+// start: entry offsets of the T own rows (natural row order); lcol: local
+// column of each entry (own rows 0..T-1, then spill targets T..W-1);
+// tcsc/tptr: the off-diagonal entries grouped by local target (CSC of the
+// tile), each as (entry index | local row << 16); tgt: global row of each
+// spill target.  K3's staging slots live outside the block (`slots`).
 struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
   int32_t nrows;        // T
   int32_t nspill;       // S (window W = T + S)
-  int32_t nnz;          // stored entries of the tile (without padding)
+  int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
+  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block (o_slot unused)
   int32_t spill_off;    // first spill entry of this tile (targets / slots arrays)
-  uint16_t o_ro, o_tt, o_rofs, o_rlen, o_cofs, o_clen, o_tc, o_lcol, o_tgt, o_val;
-  uint16_t nrs, ncs;    // row slices R, CSC slices C
-  int32_t pad[2];
+  int32_t pad[5];
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
 

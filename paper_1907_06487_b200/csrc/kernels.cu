@@ -357,51 +357,37 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
     const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
-    const uint16_t* tt = reinterpret_cast<const uint16_t*>(blk + D.o_tt);
-    const uint16_t* rofs = reinterpret_cast<const uint16_t*>(blk + D.o_rofs);
-    const uint16_t* rlen = reinterpret_cast<const uint16_t*>(blk + D.o_rlen);
-    const uint16_t* cofs = reinterpret_cast<const uint16_t*>(blk + D.o_cofs);
-    const uint16_t* clen = reinterpret_cast<const uint16_t*>(blk + D.o_clen);
-    const uint32_t* tc = reinterpret_cast<const uint32_t*>(blk + D.o_tc);
+    const uint16_t* start = reinterpret_cast<const uint16_t*>(blk + sizeof(TileDesc));
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
+    const uint32_t* tcsc = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
+    const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = A.slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    const int R = D.nrs, Cn = D.ncs;
-    // one warp per 32-target slice (SELL-32: a warp step reads 32 consecutive
-    // words); lane j of slice s owns target tt[32 s + j] (fixed order -> deterministic):
+    // one pass, one thread per local target l (fixed order -> deterministic):
     //   own row l:  sum_{e in row l} a_e x[c_e]                    (tmp)
     //   every l:    sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
-    const int gw = gt >> 5;
-    for (int sI = gw; sI < Cn; sI += kGroupWarps) {
-      const int q = sI * 32 + lane;
-      const int l = tt[q];
-      const int sl = (!ATOMIC && l != 0xffff && l >= T) ? __ldg(slot + (l - T)) : 0;
+    for (int l = gt; l < W; l += kGroupThreads) {
+      // K3: the staging slot is fetched first so its latency overlaps the sums
+      const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
       double acc = 0.0;
-      if (sI < R) {
-        const int len = rlen[q];
-        const int base = rofs[sI] + lane;
+      if (l < T) {
+        const int eb = start[l], ee = start[l + 1];
 #pragma unroll 4
-        for (int i = 0; i < len; ++i) {
-          const int f = base + 32 * i;
-          acc += val[f] * xs[lcol[f]];
-        }
+        for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
       }
-      const int len = clen[q];
-      const int cb = cofs[sI] + lane;
+      const int jb = tptr[l], je = tptr[l + 1];
 #pragma unroll 4
-      for (int i = 0; i < len; ++i) {
-        const uint32_t e = tc[cb + 32 * i];
-        acc += val[e & 0xffffu] * xs[e >> 16];
+      for (int j = jb; j < je; ++j) {
+        const uint32_t q = tcsc[j];
+        acc += val[q & 0xffffu] * xs[q >> 16];
       }
-      if (l != 0xffff) {
-        if (ATOMIC) {
-          atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
-        } else if (l < T) {
-          y[row0 + l] = acc;
-        } else {
-          __stcg(A.spill_buf + sl, acc);
-        }
+      if (ATOMIC) {
+        atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
+      } else if (l < T) {
+        y[row0 + l] = acc;
+      } else {
+        __stcg(A.spill_buf + sl, acc);
       }
     }
     if (gt == 0) TRACE(k, 4);
