@@ -5,7 +5,6 @@
 
 #include <algorithm>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -167,7 +166,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     const int64_t o_start = (int64_t)sizeof(TileDesc);
     int64_t o_lcol = align16(o_start + 2 * (int64_t)(T + 1));
     int64_t o_tidx = align16(o_lcol + 2 * nnz);
-    int64_t o_tptr = align16(o_tidx + 2 * (nnz - nd));
+    int64_t o_tptr = align16(o_tidx + 4 * (nnz - nd));
     int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
     int64_t o_slot = o_tgt;
     int64_t o_val = align16(o_tgt + 4 * (int64_t)S_);
@@ -217,7 +216,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
     uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
     uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
-    uint16_t* tcsc = reinterpret_cast<uint16_t*>(blk + D.o_tidx);
+    uint32_t* tcsc = reinterpret_cast<uint32_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
@@ -250,7 +249,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     for (int32_t l = 0; l <= W; ++l) tptr[l] = (uint16_t)tcnt[(size_t)l];
     for (int32_t r = r0; r < r1; ++r)
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
-        if (S.pcol[(size_t)i] != r) tcsc[tcnt[lcol[i - e0]]++] = (uint16_t)(i - e0);
+        if (S.pcol[(size_t)i] != r) tcsc[tcnt[lcol[i - e0]]++] = (uint32_t)(i - e0) | ((uint32_t)(r - r0) << 16);
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   // multi-rank: keep only this rank's tiles (descriptors re-based to the range)
@@ -287,7 +286,6 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   A.block_cap = block_cap;
   A.window_cap = window_cap;
   A.nnz_cap = nnz_cap;
-  if (const char* dbg = std::getenv("SYMM_DEBUG_SKIP")) A.debug_skip = std::atoi(dbg);  // diagnostics only
   P->fargs = FixupArgs{n, P->d_in_ptr, d_spill};
   int stages = 0;
   rc = tiled_max_ctas_per_sm(P->vec, A, &stages);

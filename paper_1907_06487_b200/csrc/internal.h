@@ -68,13 +68,13 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
-//   TileDesc (64 B) | start u16[T+1] | lcol u16[nnz] | tcsc u16[noff] |
+//   TileDesc (64 B) | start u16[T+1] | lcol u16[nnz] | tcsc u32[noff] |
 //   tptr u16[W+1] | tgt i32[S] | val f64[nnz]
 // start: entry offsets of the T own rows (natural row order); lcol: local
 // column of each entry (own rows 0..T-1, then spill targets T..W-1);
-// tcsc/tptr: the off-diagonal entry indices grouped by local target (CSC of
-// the tile); tgt: global row of each spill target.  K3's staging slots live
-// outside the block (`slots`).
+// tcsc/tptr: the off-diagonal entries grouped by local target (CSC of the
+// tile), each as (entry index | local row << 16); tgt: global row of each
+// spill target.  K3's staging slots live outside the block (`slots`).
 struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
@@ -98,7 +98,6 @@ struct TiledArgs {
   int32_t block_cap, window_cap, nnz_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)
   unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
-  int32_t debug_skip;             // diagnostics only (env SYMM_DEBUG_SKIP): bit0 row part, bit1 CSC part
 };
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions

@@ -347,14 +347,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // -------------------------------------------------- consumer groups
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
-  double* ys = reinterpret_cast<double*>(sm + NS * slot_bytes) + (size_t)g * (A.window_cap + A.nnz_cap);
-  double* Pp = ys + A.window_cap;
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
     mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));  // TMA data visible to this thread
     mbar_wait(&x_full[s], (unsigned)((k / NS) & 1));
-    group_sync(g);  // this group's ys/P scratch is no longer read by its previous tile
     if (gt == 0) TRACE(k, 3);
     const unsigned char* blk = sm + s * slot_bytes;
     const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
@@ -362,36 +359,29 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
     const uint16_t* start = reinterpret_cast<const uint16_t*>(blk + sizeof(TileDesc));
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
-    const uint16_t* tcsc = reinterpret_cast<const uint16_t*>(blk + D.o_tidx);
+    const uint32_t* tcsc = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = A.slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    // pass 1, one thread per own row i:   ys[i] = sum_{e in row i} a_e x[c_e]   (tmp)
-    //                                     P[e]  = a_e x[i]                       (the transposed product)
-    for (int i = gt; i < T; i += kGroupThreads) {
-      if (A.debug_skip & 1) { ys[i] = 0.0; continue; }
-      const int eb = start[i], ee = start[i + 1];
-      const double xi = xs[i];
-      double acc = 0.0;
-#pragma unroll 4
-      for (int e = eb; e < ee; ++e) {
-        const double a = val[e];
-        acc += a * xs[lcol[e]];
-        Pp[e] = a * xi;  // the diagonal's P is never read (not in the CSC lists)
-      }
-      ys[i] = acc;
-    }
-    group_sync(g);
-    // pass 2, one thread per local target l: y_l = ys[l] + sum_{e: c_e = l} P[e]
-    // (fixed order -> deterministic); then the flush
+    // one pass, one thread per local target l (fixed order -> deterministic):
+    //   own row l:  sum_{e in row l} a_e x[c_e]                    (tmp)
+    //   every l:    sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
     for (int l = gt; l < W; l += kGroupThreads) {
       // K3: the staging slot is fetched first so its latency overlaps the sums
       const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
-      double acc = l < T ? ys[l] : 0.0;
-      const int jb = tptr[l], je = (A.debug_skip & 2) ? jb : tptr[l + 1];
+      double acc = 0.0;
+      if (l < T) {
+        const int eb = start[l], ee = start[l + 1];
 #pragma unroll 4
-      for (int j = jb; j < je; ++j) acc += Pp[tcsc[j]];
+        for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
+      }
+      const int jb = tptr[l], je = tptr[l + 1];
+#pragma unroll 4
+      for (int j = jb; j < je; ++j) {
+        const uint32_t q = tcsc[j];
+        acc += val[q & 0xffffu] * xs[q >> 16];
+      }
       if (ATOMIC) {
         atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
       } else if (l < T) {
@@ -487,7 +477,7 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
 }
 
 int tiled_smem_bytes(const TiledArgs& T) {
-  return T.stages * (T.block_cap + 8 * T.window_cap) + kGroups * 8 * (T.window_cap + T.nnz_cap);
+  return T.stages * (T.block_cap + 8 * T.window_cap);
 }
 
 template <int NS>
