@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -286,6 +287,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   A.block_cap = block_cap;
   A.window_cap = window_cap;
   A.nnz_cap = nnz_cap;
+  if (const char* dbg = std::getenv("SYMM_DEBUG_SKIP")) A.debug_skip = std::atoi(dbg);  // diagnostics only
   P->fargs = FixupArgs{n, P->d_in_ptr, d_spill};
   int stages = 0;
   rc = tiled_max_ctas_per_sm(P->vec, A, &stages);

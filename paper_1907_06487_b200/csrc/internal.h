@@ -98,6 +98,8 @@ struct TiledArgs {
   int32_t block_cap, window_cap, nnz_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)
   unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
+  int32_t debug_skip;             // diagnostics only (env SYMM_DEBUG_SKIP): skip bit0 row part,
+                                  // bit1 CSC part, bit2 flush, bit3 spill-x gather (wrong results)
 };
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions

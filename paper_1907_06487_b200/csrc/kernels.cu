@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       if (lane == 0 && p == 1) cp_async8(xs, x + row0);
       if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
 #pragma unroll 4
-      for (int idx = lane; idx < S; idx += 32) cp_async8(xs + T + idx, x + tgt[idx]);
+      for (int idx = lane; idx < S && !(A.debug_skip & 8); idx += 32) cp_async8(xs + T + idx, x + tgt[idx]);
       cp_async_arrive_noinc(&x_full[s]);
       if (lane == 0) TRACE(k, 2);
     }
@@ -371,18 +371,20 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       // K3: the staging slot is fetched first so its latency overlaps the sums
       const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
       double acc = 0.0;
-      if (l < T) {
+      if (l < T && !(A.debug_skip & 1)) {
         const int eb = start[l], ee = start[l + 1];
 #pragma unroll 4
         for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
       }
-      const int jb = tptr[l], je = tptr[l + 1];
+      const int jb = tptr[l], je = (A.debug_skip & 2) ? jb : tptr[l + 1];
 #pragma unroll 4
       for (int j = jb; j < je; ++j) {
         const uint32_t q = tcsc[j];
         acc += val[q & 0xffffu] * xs[q >> 16];
       }
-      if (ATOMIC) {
+      if (A.debug_skip & 4) {
+        // diagnostics: no flush
+      } else if (ATOMIC) {
         atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
       } else if (l < T) {
         y[row0 + l] = acc;
