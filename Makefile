@@ -6,6 +6,12 @@
 NVCC ?= nvcc
 CXX ?= g++
 CC ?= gcc
+# host C++ compiler with OpenMP: the first of $(CXX), g++, /usr/bin/g++ that
+# links -fopenmp (some images point CXX at a wrapper without libgomp.spec)
+OMPCXX := $(shell for c in $(CXX) g++ /usr/bin/g++; do echo 'int main(){return 0;}' | $$c -fopenmp -x c++ - -o /dev/null >/dev/null 2>&1 && { echo $$c; break; }; done)
+ifeq ($(OMPCXX),)
+$(error no host C++ compiler with OpenMP support found)
+endif
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp,-O3 -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_1907_06487_b200
@@ -17,14 +23,14 @@ PROD_HDRS := include/symmspmv.h $(CSRC)/internal.h
 all: gen/libsymmgen.so oracle/liboracle.so $(PKG)/libsymmspmv.so
 
 gen/libsymmgen.so: gen/symmgen.cpp
-	$(CXX) -O2 -std=c++17 -fopenmp -fPIC -shared -Wall -o $@ $<
+	$(OMPCXX) -O2 -std=c++17 -fopenmp -fPIC -shared -Wall -o $@ $<
 
 # -ffp-contract=off: no FMA contraction in the oracle (reading R5)
 oracle/liboracle.so: oracle/oracle.c
 	$(CC) -O2 -std=c99 -ffp-contract=off -fPIC -shared -Wall -o $@ $<
 
 $(CSRC)/schedule.o: $(CSRC)/schedule.cpp $(PROD_HDRS)
-	$(CXX) -O3 -std=c++17 -fopenmp -fPIC -Wall -Iinclude -c -o $@ $<
+	$(OMPCXX) -O3 -std=c++17 -fopenmp -fPIC -Wall -Iinclude -c -o $@ $<
 
 $(CSRC)/capi.o: $(CSRC)/capi.cpp $(PROD_HDRS)
 	$(NVCC) $(NVFLAGS) -Iinclude -x cu -c -o $@ $<
