@@ -13,11 +13,11 @@ ifeq ($(OMPCXX),)
 $(error no host C++ compiler with OpenMP support found)
 endif
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp,-O3 -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) $(EXTRA_NVFLAGS) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp,-O3 -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_1907_06487_b200
 CSRC := $(PKG)/csrc
 
-PROD_SRCS := $(CSRC)/schedule.cpp $(CSRC)/capi.cpp $(CSRC)/kernels.cu
+PROD_SRCS := $(CSRC)/schedule.cpp $(CSRC)/cs_build.cpp $(CSRC)/capi.cpp $(CSRC)/kernels.cu
 PROD_HDRS := include/symmspmv.h $(CSRC)/internal.h
 
 all: gen/libsymmgen.so oracle/liboracle.so $(PKG)/libsymmspmv.so
@@ -32,13 +32,16 @@ oracle/liboracle.so: oracle/oracle.c
 $(CSRC)/schedule.o: $(CSRC)/schedule.cpp $(PROD_HDRS)
 	$(OMPCXX) -O3 -std=c++17 -fopenmp -fPIC -Wall -Iinclude -c -o $@ $<
 
+$(CSRC)/cs_build.o: $(CSRC)/cs_build.cpp $(PROD_HDRS)
+	$(OMPCXX) -O3 -std=c++17 -fopenmp -fPIC -Wall -Iinclude -c -o $@ $<
+
 $(CSRC)/capi.o: $(CSRC)/capi.cpp $(PROD_HDRS)
 	$(NVCC) $(NVFLAGS) -Iinclude -x cu -c -o $@ $<
 
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(PROD_HDRS)
 	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $< 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
-$(PKG)/libsymmspmv.so: $(CSRC)/schedule.o $(CSRC)/capi.o $(CSRC)/kernels.o
+$(PKG)/libsymmspmv.so: $(CSRC)/schedule.o $(CSRC)/cs_build.o $(CSRC)/capi.o $(CSRC)/kernels.o
 	$(NVCC) $(ARCH) -shared -Xcompiler -fopenmp -o $@ $^ -lcudart
 
 clean:

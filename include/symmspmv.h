@@ -143,7 +143,10 @@ typedef enum {
   SYMM_VARIANT_COLORED = 1, /* K2: one launch per phase, global read-modify-write     */
   SYMM_VARIANT_ATOMIC = 2,  /* K1: one launch, native fp64 RED for transposed updates */
   SYMM_VARIANT_TILED = 3,   /* K3: TMA-staged tiles, smem two-pass, staged fixup; deterministic */
-  SYMM_VARIANT_TILED_ATOMIC = 4 /* K4: same tiles, window flushed with fp64 RED into zeroed y */
+  SYMM_VARIANT_TILED_ATOMIC = 4,/* K4: same tiles, window flushed with fp64 RED into zeroed y */
+  SYMM_VARIANT_COLORED_SMEM = 5 /* K5: RACE write-set colours run inside a shared-memory x/y window
+                                   (plain smem read-modify-write, one barrier per colour); window
+                                   flushed with fp64 RED into zeroed y                        */
 } symm_variant;
 
 typedef enum { SYMM_ORDER_PERMUTED = 0, SYMM_ORDER_ORIGINAL = 1 } symm_vec_order;

@@ -60,6 +60,13 @@ struct symmspmv_plan {
   int tiled_occ = 0;
   int32_t* d_in_ptr = nullptr;
   FixupArgs fargs{};
+  // K5 colored_smem
+  bool has_cs = false;
+  CsArgs cargs{};
+  int cs_grid = 0;
+  int cs_occ = 0;
+  int cs_nc = 12;
+  int64_t cs_sum_colors = 0, cs_sum_spill = 0;
   // vector order / host staging
   int32_t *d_perm = nullptr, *d_inv = nullptr;
   double *d_xp = nullptr, *d_yp = nullptr;
@@ -303,6 +310,61 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   return SYMM_OK;
 }
 
+// K5 format (cs_build.cpp); single rank.
+int build_cs(symmspmv_plan_t* P, const Schedule& S) {
+  const int32_t nt = (int32_t)S.tile_group.size();
+  int32_t wcap = 4096, nnzcap = 1 << 30, chunk = 24576, nc = 8, stages = 4;
+  if (const char* v = std::getenv("SYMM_CS_WINDOW")) wcap = std::atoi(v);
+  if (const char* v = std::getenv("SYMM_CS_NNZ")) nnzcap = std::atoi(v);
+  if (const char* v = std::getenv("SYMM_CS_CHUNK")) chunk = std::atoi(v);
+  if (const char* v = std::getenv("SYMM_CS_NC")) nc = std::atoi(v);
+  if (const char* v = std::getenv("SYMM_CS_STAGES")) stages = std::atoi(v);
+  if (stages != 4 && stages != 8) return set_error(SYMM_ERR_ARG, "colored_smem ring stages %d (4 or 8)", stages);
+  int devsmem = 0;
+  cudaDeviceGetAttribute(&devsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P->device);
+  // ring stages: what is left after heads and windows (capped at kCsMaxStages = 8)
+  CsHost H;
+  int rc = build_cs_format(S, 0, nt, wcap, nnzcap, chunk, stages, &H);
+  if (rc) return rc;
+  CsArgs& A = P->cargs;
+  A.Wcap = H.Wcap;
+  A.Hcap = H.Hcap;
+  A.chunk = chunk;
+  A.stages = stages;
+  A.lgstages = stages == 8 ? 3 : 2;
+  if (H.max_colour_chunks > stages - 1)
+    return set_error(SYMM_ERR_SCHEDULE, "colored_smem: a colour spans %d chunks (ring of %d)", H.max_colour_chunks, stages);
+  if (cs_smem_bytes(A) + 1024 > devsmem)
+    return set_error(SYMM_ERR_UNSUPPORTED, "colored_smem needs %d B of shared memory (window %d, head %d, ring %d x %d)",
+                     cs_smem_bytes(A), H.Wcap, H.Hcap, stages, chunk);
+  CsDesc* d_desc;
+  unsigned char* d_blocks;
+  int64_t* d_coff;
+  int32_t* d_clen;
+  if ((rc = upload(P, &d_desc, H.desc.data(), H.desc.size())) ||
+      (rc = upload(P, &d_blocks, H.blocks.data(), H.blocks.size())) ||
+      (rc = upload(P, &d_coff, H.chunk_off.data(), H.chunk_off.size())) ||
+      (rc = upload(P, &d_clen, H.chunk_len.data(), H.chunk_len.size())))
+    return rc;
+  A.desc = d_desc;
+  A.ntiles = (int32_t)H.desc.size();
+  A.blocks = d_blocks;
+  A.chunk_off = d_coff;
+  A.chunk_len = d_clen;
+  if (const char* dbg = std::getenv("SYMM_DEBUG_SKIP")) A.debug_skip = std::atoi(dbg);  // diagnostics only
+  int occ = 0;
+  rc = cs_configure(A, &occ, nc);
+  if (rc) return cuda_fail((cudaError_t)rc, "colored_smem configure");
+  if (occ < 1) return set_error(SYMM_ERR_UNSUPPORTED, "colored_smem needs %d B of shared memory per CTA", cs_smem_bytes(A));
+  P->cs_occ = occ;
+  P->cs_nc = nc;
+  P->cs_grid = std::max(1, std::min(P->sms * occ, A.ntiles));
+  P->cs_sum_colors = H.sum_colors;
+  P->cs_sum_spill = H.sum_spill;
+  P->has_cs = true;
+  return SYMM_OK;
+}
+
 int build_colored(symmspmv_plan_t* P, const Schedule& S) {
   const int32_t nt = (int32_t)S.tile_group.size();
   std::vector<int32_t> ptiles;
@@ -359,6 +421,11 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
     if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, true, st)))
       return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
+    P->last_launches = 2;
+  } else if (variant == SYMM_VARIANT_COLORED_SMEM) {
+    if (!P->has_cs) return set_error(SYMM_ERR_ARG, "variant COLORED_SMEM was not uploaded by this plan");
+    if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    if ((rc = launch_cs(P->cargs, x, y, P->cs_grid, P->cs_nc, st))) return cuda_fail((cudaError_t)rc, "k_cs");
     P->last_launches = 2;
   } else {
     return set_error(SYMM_ERR_ARG, "unknown variant %d", variant);
@@ -532,7 +599,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   if (U && (U->n != S.n || U->nnz != S.nnz))
     return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
                      (long long)U->nnz, S.n, (long long)S.nnz);
-  if (opt.variant < 0 || opt.variant > 4) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
+  if (opt.variant < 0 || opt.variant > 5) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
   if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks)
     return set_error(SYMM_ERR_ARG, "rank %d of %d", opt.rank, opt.nranks);
   if (opt.nranks > 1 && opt.variant != SYMM_VARIANT_TILED_ATOMIC && opt.variant != SYMM_VARIANT_AUTO)
@@ -571,8 +638,9 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_TILED_ATOMIC || v == SYMM_VARIANT_AUTO;
   bool want_col = all || v == SYMM_VARIANT_COLORED;
   bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
+  bool want_cs = all || v == SYMM_VARIANT_COLORED_SMEM;
   if (opt.nranks > 1) {
-    want_col = want_csr = false;
+    want_col = want_csr = want_cs = false;
     P->variant = SYMM_VARIANT_TILED_ATOMIC;
   }
   if (want_tiled) {
@@ -595,6 +663,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
       P->has_csr = true;
   }
   if (!rc && want_col) rc = build_colored(P, S);
+  if (!rc && want_cs) rc = build_cs(P, S);
   if (!rc) {
     if (!(rc = upload(P, &P->d_perm, S.perm.data(), S.perm.size())) &&
         !(rc = upload(P, &P->d_inv, S.inv.data(), S.inv.size())) && !(rc = dev_alloc(P, &P->d_xp, (size_t)S.n)))
@@ -743,6 +812,67 @@ extern "C" int symmspmv_debug_trace(symmspmv_plan_t* P, const double* x, double*
   cudaMemcpy(host_trace, d, bytes, cudaMemcpyDeviceToHost);
   cudaFree(d);
   return rc ? cuda_fail((cudaError_t)rc, "trace launch") : SYMM_OK;
+}
+
+// Diagnostics (not in the public header): one colored_smem run with the event
+// trace of CTA 0: host_trace[2*cap] chunk (wait start, issue) times, then
+// 256 x 4 tile times (start, window ready, colours done, flush done).
+extern "C" int symm_cs_debug_trace(symmspmv_plan_t* P, const double* x, double* y, void* stream,
+                                   unsigned long long* host_trace, int32_t cap) {
+  if (!P || !P->has_cs) return set_error(SYMM_ERR_ARG, "no colored_smem plan");
+  unsigned long long* d = nullptr;
+  size_t bytes = ((size_t)cap * 2 + 256 * 4 + 512 * 4 + 64) * sizeof(unsigned long long);
+  if (cudaMalloc(&d, bytes) != cudaSuccess) return set_error(SYMM_ERR_OOM, "trace buffer");
+  cudaMemset(d, 0, bytes);
+  CsArgs A = P->cargs;
+  A.trace = d;
+  A.trace_cap = cap;
+  int rc = launch_zero(y, P->n, stream);
+  if (!rc) rc = launch_cs(A, x, y, P->cs_grid, P->cs_nc, stream);
+  cudaStreamSynchronize((cudaStream_t)stream);
+  cudaMemcpy(host_trace, d, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return rc ? cuda_fail((cudaError_t)rc, "trace launch") : SYMM_OK;
+}
+
+// Diagnostics (not in the public header): statistics of the K5 format built
+// from schedule s with window cap wcap and nnz cap nnzcap (no GPU needed).
+// out[0..10] = tiles, Wcap, sum colours, sum slices, sum lane-steps
+// (32 x longest row per slice), off-diagonal entries, sum spill targets,
+// block bytes, max colours, sum rows, Scap.
+extern "C" int symm_cs_format_stats(const race_schedule_t* s, int32_t wcap, int32_t chunk, int32_t stages, int64_t* out) {
+  if (!s || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
+  const Schedule& S = s->S;
+  CsHost H;
+  int rc = build_cs_format(S, 0, (int32_t)S.tile_group.size(), wcap, 1 << 30, chunk, stages, &H);
+  if (rc) return rc;
+  int64_t rows = 0, heads = 0;
+  for (const CsDesc& D : H.desc) { rows += D.T; heads += D.head_bytes; }
+  int64_t v[13] = {(int64_t)H.desc.size(), H.Wcap, H.sum_colors, H.sum_slices, H.steps, H.nnz_offdiag, H.sum_spill,
+                   (int64_t)H.blocks.size(), H.max_colour_chunks, rows, H.conflicts, heads, H.Hcap};
+  for (int i = 0; i < 13; ++i) out[i] = v[i];
+  return SYMM_OK;
+}
+
+// Diagnostics (not in the public header): the K5 format itself, for the CPU
+// decoder test (tests/test_cs_format.py).  Call with NULL arrays to get
+// sizes[0..2] = tiles, chunks, block bytes; then with arrays of those sizes.
+extern "C" int symm_cs_format_dump(const race_schedule_t* s, int32_t wcap, int32_t chunk, int32_t stages,
+                                   int64_t* sizes, void* desc, int64_t* chunk_off, int32_t* chunk_len,
+                                   unsigned char* blocks) {
+  if (!s || !sizes) return set_error(SYMM_ERR_ARG, "NULL argument");
+  const Schedule& S = s->S;
+  CsHost H;
+  int rc = build_cs_format(S, 0, (int32_t)S.tile_group.size(), wcap, 1 << 30, chunk, stages, &H);
+  if (rc) return rc;
+  sizes[0] = (int64_t)H.desc.size();
+  sizes[1] = (int64_t)H.chunk_off.size();
+  sizes[2] = (int64_t)H.blocks.size();
+  if (desc) std::memcpy(desc, H.desc.data(), H.desc.size() * sizeof(CsDesc));
+  if (chunk_off) std::memcpy(chunk_off, H.chunk_off.data(), H.chunk_off.size() * sizeof(int64_t));
+  if (chunk_len) std::memcpy(chunk_len, H.chunk_len.data(), H.chunk_len.size() * sizeof(int32_t));
+  if (blocks) std::memcpy(blocks, H.blocks.data(), H.blocks.size());
+  return SYMM_OK;
 }
 
 int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n) {

@@ -124,6 +124,65 @@ struct ColoredArgs {
   const int32_t* sub_ptr;      // per tile colour pointers, relative to tile row start
 };
 
+// ---- K5 colored_smem (cs_build.cpp / kernels.cu) ------------------------------
+// One tile = consecutive schedule tiles of one level group; rows coloured by
+// write sets (RACE distance-2) and executed colour by colour
+// inside a shared-memory window of x and y (see cs_build.cpp for the block).
+constexpr int kCsReleaseUnits = 4096;  // ring_empty arrivals per chunk (piece weights sum to it)
+struct CsDesc {      // global descriptor of one tile (read by the head producer)
+  int64_t head_off;  // byte offset of the tile's head in `blocks`
+  int32_t head_bytes, row0, T, S, ncolors, nslices, npieces, nchunks;
+  int32_t block_bytes;  // head + chunks (the tile's block is contiguous)
+  uint16_t o_cslc, o_srec, o_ploc, o_pw, o_tgt, o_clen, pad[4];
+};
+static_assert(sizeof(CsDesc) == 64, "CsDesc must be 64 B");
+struct CsHeadHdr {   // first bytes of every head (read from shared memory)
+  int64_t chunk_base;  // byte offset of the tile's first chunk in `blocks` (chunks are contiguous)
+  int32_t row0, T, S, ncolors, nslices, npieces, nchunks;
+  uint16_t o_cslc, o_srec, o_ploc, o_pw, o_tgt, o_clen;
+  int32_t pad[4];
+};
+static_assert(sizeof(CsHeadHdr) == 64, "CsHeadHdr must be 64 B");
+struct CsSliceRec {  // one slice (<= 32 rows of one colour), 16 B
+  uint32_t ploc0;    // location of its first piece ((chunk in tile << 20) | offset)
+  uint16_t p0;       // index of its first piece
+  uint16_t nsteps;   // longest row (off-diagonal entries) = JDS steps
+  uint8_t npieces, m, pad[6];
+};
+static_assert(sizeof(CsSliceRec) == 16, "CsSliceRec must be 16 B");
+
+struct CsHost {
+  std::vector<CsDesc> desc;
+  std::vector<int64_t> chunk_off;   // byte offset of every chunk (tiles in order)
+  std::vector<int32_t> chunk_len;   // bytes of every chunk (multiple of 16)
+  std::vector<int32_t> tile_chunk0; // first chunk of every tile
+  std::vector<unsigned char> blocks;
+  int32_t Wcap = 16, Hcap = 16, max_colour_chunks = 1;
+  int64_t nnz_offdiag = 0, sum_colors = 0, sum_slices = 0, sum_spill = 0, conflicts = 0, steps = 0;
+};
+int32_t color_rows_writeset(const int32_t* rp, const int32_t* pc, int32_t r0, int32_t r1,
+                            const std::vector<int32_t>& tgt, std::vector<int32_t>& color);
+int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t wcap, int32_t nnzcap,
+                    int32_t chunk_bytes, int32_t stages, CsHost* out);
+
+struct CsArgs {
+  const CsDesc* desc;
+  int32_t ntiles;
+  const unsigned char* blocks;
+  const int64_t* chunk_off;
+  const int32_t* chunk_len;
+  int32_t Wcap, Hcap;             // window entries, head bytes (capacities of the smem buffers)
+  int32_t chunk;                  // bytes of one ring stage
+  int32_t stages;                 // ring depth (power of two)
+  int32_t lgstages;               // log2(stages)
+  int32_t debug_skip;             // diagnostics (env SYMM_DEBUG_SKIP): bit0 entries, bit2 flush, bit3 stream only
+  unsigned long long* trace;      // diagnostics: CTA 0 event times (nullptr = off), see k_cs
+  int32_t trace_cap;              // chunk events [0, cap) x 2, then tile events x 4
+};
+int cs_smem_bytes(const CsArgs& A);
+int cs_configure(CsArgs& A, int* ctas_per_sm, int nc);   // sets the smem attribute, returns occupancy
+int launch_cs(const CsArgs& A, const double* x, double* y, int grid, int nc, void* stream);
+
 // kernel launchers (kernels.cu); return cudaError_t as int
 int launch_zero(double* y, int64_t n, void* stream);
 int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream);

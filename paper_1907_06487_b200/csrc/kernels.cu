@@ -185,6 +185,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
   asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -413,6 +416,290 @@ __global__ void __launch_bounds__(256) k_fixup(FixupArgs F, double* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- K5 colored_smem
+// RACE colouring executed inside a shared-memory window (format: cs_build.cpp).
+// One persistent CTA per SM takes the tiles blockIdx.x, +gridDim.x, ... in
+// BFS order.  Warp roles:
+//   head producer (lane 0 of warp 1): one bulk copy (TMA, cp.async.bulk) per
+//     tile head into a double-buffered head area, as soon as the tile two
+//     back is finished;
+//   chunk producer (lane 0 of warp 0): one bulk copy per chunk of the tile's
+//     entry pieces into a kStages-deep ring (mbarrier full/empty); chunk
+//     offsets and sizes come from the head in shared memory (no global loads
+//     on the producer's critical path);
+//   2 gather warps (tiles alternate between them): x of the tile window (own
+//     rows row0.., then the spill targets) into a double-buffered xs, with
+//     cp.async, while the consumers still work on the previous tile;
+//   NC consumer warps: ys = 0; colour by colour (colours in
+//     sequence, one barrier between them), one lane per row of the colour:
+//         acc = d_r x_r + sum_j a_rj xs[c_j]          (Alg. 2 tmp)
+//         ys[c_j] += a_rj x_r                          (Alg. 2 b[col] +=)
+//         ys[r]  += acc
+//     plain shared-memory read-modify-writes: rows of one colour have disjoint
+//     write sets; the step order of every row makes the
+//     16 lanes of a half warp hit 16 different bank pairs; then the window is
+//     flushed, y[global(l)] += ys[l] (fp64 RED: other tiles share rows).
+constexpr int kCsMaxStages = 8;
+#ifdef CS_PROF
+#define CSP_DECL long long csp_acc[10] = {0}; long long csp_t = clock64();
+#define CSP(i) do { const long long _n = clock64(); csp_acc[i] += _n - csp_t; csp_t = _n; } while (0)
+#define CSP_CNT(i) (csp_acc[i]++)
+#else
+#define CSP_DECL
+#define CSP(i) do {} while (0)
+#define CSP_CNT(i) do {} while (0)
+#endif
+
+__device__ __forceinline__ void prefetch_l2(const void* p, int64_t bytes) {
+  if (bytes <= 0) return;
+  const uintptr_t a = (uintptr_t)p & ~uintptr_t(15);
+  const uintptr_t e = ((uintptr_t)p + (uintptr_t)bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+constexpr int kCsGather = 2;
+constexpr int kCsRoleWarps = 2 + kCsGather;  // chunk producer, head producer, gather warps
+
+__device__ __forceinline__ void cs_cbar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// NU (4, 8, 12 or 16) JDS steps of one piece, straight-line: every lane reads
+// an entry at every step (start of step u's run + lane); lanes whose row is
+// shorter are redirected to the zero dummy slot `dummy` with a = 0.  The
+// columns of one row are distinct and rows of one colour are write-disjoint,
+// so all loads of y can precede all stores.
+template <int NU>
+__device__ __forceinline__ void cs_steps(const double* __restrict__ val, const uint16_t* __restrict__ lc,
+                                         const uint32_t (&ew)[8], int j0, int L, int lane,
+                                         const double* __restrict__ xs, double* ys, double xr, int dummy,
+                                         double (&acc)[4]) {
+  double a[NU], xv[NU], yv[NU];
+  int c[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    const int e0 = u == 0 ? 0 : (int)((ew[(u - 1) >> 1] >> (((u - 1) & 1) * 16)) & 0xffffu);
+    const bool v = L > j0 + u;
+    const double a0 = val[e0 + lane];
+    const int c0 = lc[e0 + lane];
+    a[u] = v ? a0 : 0.0;
+    c[u] = v ? c0 : dummy;
+  }
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    xv[u] = xs[c[u]];
+    yv[u] = ys[c[u]];
+  }
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    acc[u & 3] = fma(a[u], xv[u], acc[u & 3]);
+    ys[c[u]] = fma(a[u], xr, yv[u]);
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(32 * (kCsRoleWarps + NC), 1)
+    k_cs(
+
+
+CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t head_full[2], head_empty[2], x_full[2], x_empty[2];
+  __shared__ __align__(8) uint64_t ring_full[kCsMaxStages], ring_empty[kCsMaxStages];
+  const int NS = A.stages;
+  const int Hb = (A.Hcap + 127) & ~127;
+  const int Wc = (A.Wcap + 15) & ~15;  // window slots; slot Wc is a zero dummy
+  const int Ws = Wc + 16;
+  unsigned char* heads = sm;
+  double* xs0 = reinterpret_cast<double*>(sm + 2 * Hb);
+  double* ys = xs0 + 2 * Ws;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(ys + Ws);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x;
+  const int nk = A.ntiles > (int)blockIdx.x ? (A.ntiles - (int)blockIdx.x + G - 1) / G : 0;
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&head_full[i], 1);
+      mbar_init(&head_empty[i], 1);
+      mbar_init(&x_full[i], 32);
+      mbar_init(&x_empty[i], 1);
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&ring_full[i], 1);
+      mbar_init(&ring_empty[i], kCsReleaseUnits);  // piece weights of a chunk sum to this
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    xs0[Wc] = 0.0;
+    xs0[Ws + Wc] = 0.0;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    // ------------------------------------------------ chunk producer (TMA bulk copies)
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t cseq = 0;
+      for (int k = 0; k < nk; ++k) {
+        const int hb = k & 1;
+        mbar_wait(&head_full[hb], (unsigned)((k >> 1) & 1));
+        const CsHeadHdr* H = reinterpret_cast<const CsHeadHdr*>(heads + hb * Hb);
+        const int nch = H->nchunks;
+        const uint32_t* clen = reinterpret_cast<const uint32_t*>(heads + hb * Hb + H->o_clen);
+        int64_t off = H->chunk_base;
+        for (int c = 0; c < nch; ++c, ++cseq) {
+          const int st = (int)(cseq & (uint32_t)(NS - 1));
+          const uint32_t use = cseq >> A.lgstages;
+          const unsigned len = clen[c];
+          if (A.trace && blockIdx.x == 0 && cseq < (uint32_t)A.trace_cap) A.trace[2 * cseq] = gtimer();
+          if (use > 0) mbar_wait(&ring_empty[st], (use - 1) & 1);
+          if (A.trace && blockIdx.x == 0 && cseq < (uint32_t)A.trace_cap) A.trace[2 * cseq + 1] = gtimer();
+          mbar_arrive_expect_tx(&ring_full[st], len);
+          bulk_g2s_stream(ring + (size_t)st * A.chunk, A.blocks + off, len, &ring_full[st], pol);
+          off += len;
+        }
+      }
+    }
+    return;
+  }
+  if (wid == 1) {
+    // ------------------------------------------------ head producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int k = 0; k < nk; ++k) {
+        const CsDesc* D = A.desc + blockIdx.x + (size_t)k * G;
+        const int hb = k & 1;
+        const int64_t hoff = __ldg(&D->head_off);
+        const int hbytes = __ldg(&D->head_bytes), bbytes = __ldg(&D->block_bytes);
+        if (k >= 2) mbar_wait(&head_empty[hb], (unsigned)(((k >> 1) - 1) & 1));
+        mbar_arrive_expect_tx(&head_full[hb], (unsigned)hbytes);
+        bulk_g2s_stream(heads + hb * Hb, A.blocks + hoff, (unsigned)hbytes, &head_full[hb], pol);
+        // the whole tile into L2 now (about one tile ahead of its consumption):
+        // the ring's bulk copies then hit L2 and need far fewer bytes in flight
+        if (!(A.debug_skip & 16))
+          for (int64_t o = hbytes; o < bbytes; o += 32768)
+            prefetch_l2(A.blocks + hoff + o, min((int64_t)32768, (int64_t)bbytes - o));
+      }
+    }
+    return;
+  }
+  if (wid < kCsRoleWarps) {
+    // ------------------------------------------------ gather warps (x windows)
+    const int gw = wid - 2;
+    for (int k = gw; k < nk; k += kCsGather) {
+      const int xb = k & 1;
+      mbar_wait(&head_full[xb], (unsigned)((k >> 1) & 1));
+      if (k >= 2) mbar_wait(&x_empty[xb], (unsigned)(((k >> 1) - 1) & 1));
+      const CsHeadHdr* H = reinterpret_cast<const CsHeadHdr*>(heads + xb * Hb);
+      const int row0 = H->row0, T = H->T, S = H->S;
+      const int32_t* tgt = reinterpret_cast<const int32_t*>(heads + xb * Hb + H->o_tgt);
+      double* xsb = xs0 + xb * Ws;
+      if (!(A.debug_skip & 32)) {
+        for (int i = lane; i < T; i += 32) cp_async8(xsb + i, x + row0 + i);
+#pragma unroll 4
+        for (int i = lane; i < S; i += 32) cp_async8(xsb + T + i, x + tgt[i]);
+      }
+      cp_async_arrive_noinc(&x_full[xb]);
+    }
+    return;
+  }
+  // -------------------------------------------------- consumers
+  constexpr int NCT = NC * 32;
+  const int cw = wid - kCsRoleWarps, ct = tid - 32 * kCsRoleWarps;
+  const int smask = NS - 1;
+  uint32_t cbase = 0;
+  CSP_DECL
+  for (int k = 0; k < nk; ++k) {
+    const int hb = k & 1;
+    unsigned long long* tr = (A.trace && blockIdx.x == 0 && ct == 0 && k < 256) ? A.trace + 2 * A.trace_cap + 4 * k : nullptr;
+    if (tr) tr[0] = gtimer();
+    mbar_wait(&head_full[hb], (unsigned)((k >> 1) & 1));
+    const unsigned char* hd = heads + hb * Hb;
+    const CsHeadHdr* H = reinterpret_cast<const CsHeadHdr*>(hd);
+    const int row0 = H->row0, T = H->T, S = H->S, nc = H->ncolors, nch = H->nchunks;
+    const uint16_t* cslc = reinterpret_cast<const uint16_t*>(hd + H->o_cslc);
+    const uint4* srec = reinterpret_cast<const uint4*>(hd + H->o_srec);
+    const uint32_t* ploc = reinterpret_cast<const uint32_t*>(hd + H->o_ploc);
+    const uint16_t* pw = reinterpret_cast<const uint16_t*>(hd + H->o_pw);
+    const int32_t* tgt = reinterpret_cast<const int32_t*>(hd + H->o_tgt);
+    for (int i = ct; i < T + S; i += NCT) ys[i] = 0.0;
+    mbar_wait(&x_full[hb], (unsigned)((k >> 1) & 1));
+    const double* xsb = xs0 + hb * Ws;
+    cs_cbar(NCT);
+    if (tr) tr[1] = gtimer();
+    CSP(6);
+    for (int kk = 0; kk < nc; ++kk) {
+      const int s1 = cslc[kk + 1];
+      for (int s = cslc[kk] + cw; s < s1; s += NC) {
+        const uint4 rec = srec[s];  // CsSliceRec
+        const uint32_t ploc0 = rec.x;
+        const int p0 = (int)(rec.y & 0xffffu), nsteps = (int)(rec.y >> 16);
+        const int npc = (int)(rec.z & 0xffu), m = (int)((rec.z >> 8) & 0xffu);
+        int L = 0, lr = 0;
+        double d = 0.0, xr = 0.0;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        CSP(0);
+        for (int kp = 0; kp < npc; ++kp) {
+          const uint32_t loc = kp == 0 ? ploc0 : ploc[p0 + kp];
+          const uint32_t ch = cbase + (loc >> 20);
+          const int st = (int)(ch & (uint32_t)smask);
+          mbar_wait(&ring_full[st], (ch >> A.lgstages) & 1);
+          CSP(1);
+          const unsigned char* b = ring + (size_t)st * A.chunk + (loc & 0xfffffu);
+          const uint4 e0 = reinterpret_cast<const uint4*>(b)[0];  // eo[0..7]
+          const uint4 e1 = reinterpret_cast<const uint4*>(b)[1];  // eo[8..15]
+          const uint32_t ew[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+          const int nnzp = (int)(e1.w >> 16);
+          if (kp == 0) {  // the slice's rows: window id, length, diagonal (zeros past m)
+            lr = reinterpret_cast<const uint16_t*>(b + 32)[lane];
+            L = reinterpret_cast<const uint16_t*>(b + 96)[lane];
+            d = reinterpret_cast<const double*>(b + 160)[lane];
+            if (A.debug_skip & 1) L = 0;
+            xr = xsb[lr];
+            b += 416;
+          } else {
+            b += 32;
+          }
+          const double* val = reinterpret_cast<const double*>(b);
+          const uint16_t* lc = reinterpret_cast<const uint16_t*>(b + 8 * nnzp);
+          const int j0 = kp * 16, nst = min(16, nsteps - j0);
+          switch ((nst + 3) >> 2) {
+            case 4: cs_steps<16>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
+            case 3: cs_steps<12>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
+            case 2: cs_steps<8>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
+            case 1: cs_steps<4>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
+            default: break;
+          }
+          CSP(2);
+          __syncwarp();  // every lane is done with the piece: release its share of the stage
+          if (lane == 0) mbar_arrive_cnt(&ring_empty[st], pw[p0 + kp]);
+          CSP(3);
+          CSP_CNT(8);
+        }
+        if (lane < m) ys[lr] += fma(d, xr, (acc[0] + acc[1]) + (acc[2] + acc[3]));
+        CSP(4);
+        CSP_CNT(9);
+      }
+      cs_cbar(NCT);
+      CSP(5);
+    }
+    if (tr) tr[2] = gtimer();
+    // flush (the head's tgt list is still valid: head_empty is released below)
+    if (!(A.debug_skip & 4)) {
+      for (int i = ct; i < T; i += NCT) atomicAdd(y + row0 + i, ys[i]);
+      for (int i = ct; i < S; i += NCT) atomicAdd(y + tgt[i], ys[T + i]);
+    }
+    cs_cbar(NCT);
+    if (tr) tr[3] = gtimer();
+    CSP(7);
+    if (ct == 0) {
+      mbar_arrive(&head_empty[hb]);
+      mbar_arrive(&x_empty[hb]);
+    }
+    cbase += (uint32_t)nch;
+  }
+#ifdef CS_PROF
+  if (lane == 0 && A.trace) for (int i = 0; i < 10; ++i) atomicAdd(A.trace + 2 * A.trace_cap + 1024 + 2048 + i, (unsigned long long)csp_acc[i]);
+#endif
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -532,6 +819,42 @@ int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int gr
     default: return (int)cudaErrorInvalidValue;
   }
 #undef LT
+  return (int)cudaGetLastError();
+}
+
+
+int cs_smem_bytes(const CsArgs& A) {
+  const int64_t Hb = (A.Hcap + 127) & ~127, Ws = ((A.Wcap + 15) & ~15) + 16;
+  return (int)(2 * Hb + 24 * Ws + (int64_t)A.stages * A.chunk + 1024);  // + over-read pad of the ring
+}
+
+#define CS_INSTANCES(X) X(8) X(12) X(16)
+
+int cs_configure(CsArgs& A, int* ctas_per_sm, int nc) {
+  const int smem = cs_smem_bytes(A);
+  int devsmem = 0;
+  cudaDeviceGetAttribute(&devsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+  *ctas_per_sm = 0;
+  if (smem + 1024 > devsmem || A.stages > kCsMaxStages) return 0;
+  int rc = (int)cudaErrorInvalidValue;
+#define CS_CFG(NN)                                                                                    \
+  if (nc == NN) {                                                                                     \
+    rc = (int)cudaFuncSetAttribute(k_cs<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+    if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k_cs<NN>, 32 * (kCsRoleWarps + NN), smem); \
+  }
+  CS_INSTANCES(CS_CFG)
+#undef CS_CFG
+  return rc;
+}
+
+int launch_cs(const CsArgs& A, const double* x, double* y, int grid, int nc, void* stream) {
+  if (A.ntiles <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int smem = cs_smem_bytes(A);
+#define CS_LAUNCH(NN) \
+  if (nc == NN) k_cs<NN><<<grid, 32 * (kCsRoleWarps + NN), smem, st>>>(A, x, y);
+  CS_INSTANCES(CS_LAUNCH)
+#undef CS_LAUNCH
   return (int)cudaGetLastError();
 }
 
