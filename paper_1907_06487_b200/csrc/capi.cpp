@@ -313,18 +313,19 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
 // K5 format (cs_build.cpp); single rank.
 int build_cs(symmspmv_plan_t* P, const Schedule& S) {
   const int32_t nt = (int32_t)S.tile_group.size();
-  int32_t wcap = 4096, nnzcap = 1 << 30, chunk = 24576, nc = 8, stages = 4;
+  int32_t wcap = 4096, nnzcap = 1 << 30, chunk = 24576, nc = 8, stages = 4, V = 1;
   if (const char* v = std::getenv("SYMM_CS_WINDOW")) wcap = std::atoi(v);
   if (const char* v = std::getenv("SYMM_CS_NNZ")) nnzcap = std::atoi(v);
   if (const char* v = std::getenv("SYMM_CS_CHUNK")) chunk = std::atoi(v);
   if (const char* v = std::getenv("SYMM_CS_NC")) nc = std::atoi(v);
   if (const char* v = std::getenv("SYMM_CS_STAGES")) stages = std::atoi(v);
+  if (const char* v = std::getenv("SYMM_CS_V")) V = std::atoi(v);
   if (stages != 4 && stages != 8) return set_error(SYMM_ERR_ARG, "colored_smem ring stages %d (4 or 8)", stages);
   int devsmem = 0;
   cudaDeviceGetAttribute(&devsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P->device);
   // ring stages: what is left after heads and windows (capped at kCsMaxStages = 8)
   CsHost H;
-  int rc = build_cs_format(S, 0, nt, wcap, nnzcap, chunk, stages, &H);
+  int rc = build_cs_format(S, 0, nt, wcap, nnzcap, chunk, stages, V, &H);
   if (rc) return rc;
   CsArgs& A = P->cargs;
   A.Wcap = H.Wcap;
@@ -332,6 +333,7 @@ int build_cs(symmspmv_plan_t* P, const Schedule& S) {
   A.chunk = chunk;
   A.stages = stages;
   A.lgstages = stages == 8 ? 3 : 2;
+  A.lgv = V == 4 ? 2 : V == 2 ? 1 : 0;
   if (H.max_colour_chunks > stages - 1)
     return set_error(SYMM_ERR_SCHEDULE, "colored_smem: a colour spans %d chunks (ring of %d)", H.max_colour_chunks, stages);
   if (cs_smem_bytes(A) + 1024 > devsmem)
@@ -462,7 +464,7 @@ void race_config_default(race_config* c) {
   std::memset(c, 0, sizeof *c);
   c->k = 2;
   c->n_workers = 0;
-  c->tile_work = 1792;
+  c->tile_work = 3500;  // measured on B200 (profiles/r1_summary.md): bigger tiles, fewer spill REDs
   c->balance_by = 1;
   c->root = -1;
   c->n_eps = 3;
@@ -470,8 +472,8 @@ void race_config_default(race_config* c) {
   c->eps[1] = 0.8;
   for (int i = 2; i < 8; ++i) c->eps[i] = 0.5;
   c->max_tile_rows = 1024;
-  c->max_tile_window = 768;
-  c->max_tile_nnz = 1536;
+  c->max_tile_window = 1200;
+  c->max_tile_nnz = 3000;
   c->reorder = 1;
   c->cone_tiles = 0;
   c->min_group_levels = 2;
@@ -840,11 +842,12 @@ extern "C" int symm_cs_debug_trace(symmspmv_plan_t* P, const double* x, double* 
 // out[0..10] = tiles, Wcap, sum colours, sum slices, sum lane-steps
 // (32 x longest row per slice), off-diagonal entries, sum spill targets,
 // block bytes, max colours, sum rows, Scap.
-extern "C" int symm_cs_format_stats(const race_schedule_t* s, int32_t wcap, int32_t chunk, int32_t stages, int64_t* out) {
+extern "C" int symm_cs_format_stats(const race_schedule_t* s, int32_t wcap, int32_t chunk, int32_t stages, int32_t V,
+                                    int64_t* out) {
   if (!s || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
   const Schedule& S = s->S;
   CsHost H;
-  int rc = build_cs_format(S, 0, (int32_t)S.tile_group.size(), wcap, 1 << 30, chunk, stages, &H);
+  int rc = build_cs_format(S, 0, (int32_t)S.tile_group.size(), wcap, 1 << 30, chunk, stages, V, &H);
   if (rc) return rc;
   int64_t rows = 0, heads = 0;
   for (const CsDesc& D : H.desc) { rows += D.T; heads += D.head_bytes; }
@@ -857,13 +860,13 @@ extern "C" int symm_cs_format_stats(const race_schedule_t* s, int32_t wcap, int3
 // Diagnostics (not in the public header): the K5 format itself, for the CPU
 // decoder test (tests/test_cs_format.py).  Call with NULL arrays to get
 // sizes[0..2] = tiles, chunks, block bytes; then with arrays of those sizes.
-extern "C" int symm_cs_format_dump(const race_schedule_t* s, int32_t wcap, int32_t chunk, int32_t stages,
+extern "C" int symm_cs_format_dump(const race_schedule_t* s, int32_t wcap, int32_t chunk, int32_t stages, int32_t V,
                                    int64_t* sizes, void* desc, int64_t* chunk_off, int32_t* chunk_len,
                                    unsigned char* blocks) {
   if (!s || !sizes) return set_error(SYMM_ERR_ARG, "NULL argument");
   const Schedule& S = s->S;
   CsHost H;
-  int rc = build_cs_format(S, 0, (int32_t)S.tile_group.size(), wcap, 1 << 30, chunk, stages, &H);
+  int rc = build_cs_format(S, 0, (int32_t)S.tile_group.size(), wcap, 1 << 30, chunk, stages, V, &H);
   if (rc) return rc;
   sizes[0] = (int64_t)H.desc.size();
   sizes[1] = (int64_t)H.chunk_off.size();

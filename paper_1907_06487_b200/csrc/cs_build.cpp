@@ -101,34 +101,43 @@ int32_t color_rows_writeset(const int32_t* rp, const int32_t* pc, int32_t r0, in
 
 namespace {
 
-// Bank-aware step order of one slice (lane i = row i, entry j of row i at step
-// j): the rows' entry lists are reordered in place so that at every step the
-// active lanes of each half warp use distinct banks (window id mod 16) where
+// Bank-aware step order of one slice with V lanes per row (lane = i * V +
+// sub; entry t * V + sub of row i is handled by lane (i, sub) at step t): the
+// rows' entry lists are reordered in place so that at every step the active
+// lanes of each half warp use distinct banks (window id mod 16) where
 // possible: per (step, half) a bipartite matching lane -> bank over the
 // entries the lane's row has left (augmenting paths).  Returns the number of
 // (step, half) pairs that still conflict.
-int64_t bank_order(std::vector<std::vector<Ent>>& ent) {
+int64_t bank_order(std::vector<std::vector<Ent>>& ent, int V) {
   const int m = (int)ent.size();
   int maxlen = 0;
   for (auto& e : ent) maxlen = std::max(maxlen, (int)e.size());
+  const int nsteps = (maxlen + V - 1) / V;
   int64_t conflicts = 0;
   std::vector<char> seen(16);
-  for (int j = 0; j < maxlen; ++j) {
+  std::vector<Ent> rest;
+  for (int t = 0; t < nsteps; ++t) {
     for (int h = 0; h < 2; ++h) {
-      int lanes[16], nl = 0;
-      for (int i = 16 * h; i < std::min(m, 16 * h + 16); ++i)
-        if ((int)ent[(size_t)i].size() > j) lanes[nl++] = i;
+      int lrow[16], lsub[16], nl = 0;  // active lanes of this half
+      for (int ln = 16 * h; ln < 16 * h + 16; ++ln) {
+        const int i = ln / V, sub = ln % V;
+        if (i < m && (int)ent[(size_t)i].size() > t * V + sub) {
+          lrow[nl] = i;
+          lsub[nl] = sub;
+          ++nl;
+        }
+      }
       if (!nl) continue;
       int owner[16];
       std::fill(owner, owner + 16, -1);
       std::function<bool(int)> aug = [&](int li) -> bool {
-        auto& e = ent[(size_t)lanes[li]];
-        for (size_t q = (size_t)j; q < e.size(); ++q) {
-          const int b = e[q].first & 15;
-          if (seen[(size_t)b]) continue;
-          seen[(size_t)b] = 1;
-          if (owner[b] < 0 || aug(owner[b])) {
-            owner[b] = li;
+        auto& e = ent[(size_t)lrow[li]];
+        for (size_t q = (size_t)t * V; q < e.size(); ++q) {
+          const int bk = e[q].first & 15;
+          if (seen[(size_t)bk]) continue;
+          seen[(size_t)bk] = 1;
+          if (owner[bk] < 0 || aug(owner[bk])) {
+            owner[bk] = li;
             return true;
           }
         }
@@ -140,15 +149,41 @@ int64_t bank_order(std::vector<std::vector<Ent>>& ent) {
         matched += aug(li) ? 1 : 0;
       }
       conflicts += (matched < nl);
-      for (int b = 0; b < 16; ++b)
-        if (owner[b] >= 0) {
-          auto& e = ent[(size_t)lanes[owner[b]]];
-          for (size_t q = (size_t)j; q < e.size(); ++q)
-            if ((e[q].first & 15) == b) {
-              std::swap(e[(size_t)j], e[q]);
-              break;
-            }
-        }
+      int bank_of[16];
+      std::fill(bank_of, bank_of + 16, -1);
+      for (int bk = 0; bk < 16; ++bk)
+        if (owner[bk] >= 0) bank_of[owner[bk]] = bk;
+      // place row by row: matched lanes take an entry of their bank, the
+      // others any remaining entry; the rest keeps its order after them
+      for (int li = 0; li < nl;) {
+        const int i = lrow[li];
+        int lj = li;
+        while (lj < nl && lrow[lj] == i) ++lj;
+        auto& e = ent[(size_t)i];
+        rest.assign(e.begin() + (size_t)t * V, e.end());
+        Ent placed[16];
+        bool got[16] = {false};
+        for (int k = li; k < lj; ++k)
+          if (bank_of[k] >= 0)
+            for (size_t q = 0; q < rest.size(); ++q)
+              if ((rest[q].first & 15) == bank_of[k]) {
+                placed[lsub[k]] = rest[q];
+                got[lsub[k]] = true;
+                rest.erase(rest.begin() + (long)q);
+                break;
+              }
+        for (int k = li; k < lj; ++k)
+          if (!got[lsub[k]]) {
+            placed[lsub[k]] = rest.front();
+            got[lsub[k]] = true;
+            rest.erase(rest.begin());
+          }
+        size_t w = (size_t)t * V;
+        for (int k = li; k < lj; ++k) e[w + (size_t)lsub[k]] = placed[lsub[k]];
+        w += (size_t)(lj - li);
+        for (auto& r : rest) e[w++] = r;
+        li = lj;
+      }
     }
   }
   return conflicts;
@@ -157,7 +192,9 @@ int64_t bank_order(std::vector<std::vector<Ent>>& ent) {
 }  // namespace
 
 int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t wcap, int32_t nnzcap,
-                    int32_t chunk_bytes, int32_t stages, CsHost* out) {
+                    int32_t chunk_bytes, int32_t stages, int32_t V, CsHost* out) {
+  if (V != 1 && V != 2 && V != 4) return set_error(SYMM_ERR_ARG, "lanes per row %d (1, 2 or 4)", V);
+  const int32_t R = 32 / V;  // rows per slice
   const int32_t* rp = S.prow_ptr.data();
   const int32_t* pc = S.pcol.data();
   const double* pv = S.pval.data();
@@ -248,7 +285,7 @@ int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t w
       if (ca != cb) return ca < cb;
       return offd(a) > offd(b);
     });
-    // slices of <= 32 slots inside a colour; a colour is split before a slice
+    // slices of <= R slots inside a colour; a colour is split before a slice
     // that would push its bytes past colour_cap
     std::vector<int32_t> sl_begin, sl_end;
     X.cslc.push_back(0);
@@ -258,11 +295,11 @@ int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t w
         int32_t q = p;
         while (q < T && color[(size_t)(rows[(size_t)q] - r0)] == c) ++q;
         int64_t acc = 0;
-        for (int32_t s0 = p; s0 < q; s0 += 32) {
-          const int32_t s1 = std::min(s0 + 32, q);
+        for (int32_t s0 = p; s0 < q; s0 += R) {
+          const int32_t s1 = std::min(s0 + R, q);
           int64_t b = kSliceMeta;
           for (int32_t u = s0; u < s1; ++u) b += 10 * (int64_t)offd(rows[(size_t)u]);
-          b += 48 * (1 + offd(rows[(size_t)s0]) / kPieceSteps);
+          b += 48 * (1 + offd(rows[(size_t)s0]) / (V * kPieceSteps));
           if (acc > 0 && acc + b > colour_cap) {
             X.cslc.push_back((int32_t)sl_begin.size());  // split the colour here
             acc = 0;
@@ -300,22 +337,29 @@ int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t w
         for (int32_t i = rp[r] + (has_diag(r) ? 1 : 0); i < rp[r + 1]; ++i) e.push_back({(uint16_t)local(pc[i]), pv[i]});
         maxlen = std::max(maxlen, (int32_t)e.size());
       }
-      X.conflicts += bank_order(ent);
-      X.steps += 2 * maxlen;
-      const int32_t npc = std::max(1, (maxlen + kPieceSteps - 1) / kPieceSteps);
-      if (npc > 255 || maxlen > 255 * kPieceSteps) bad |= 4;
-      CsSliceRec R{};
-      R.p0 = (uint16_t)X.ploc.size();
-      R.npieces = (uint8_t)npc;
-      R.nsteps = (uint16_t)maxlen;
-      R.m = (uint8_t)m;
+      X.conflicts += bank_order(ent, V);
+      const int32_t nsteps = (maxlen + V - 1) / V;
+      X.steps += 2 * nsteps;
+      // lane (i, sub) holds entry t * V + sub of row i at step t
+      auto valid = [&](int32_t ln, int32_t t) {
+        const int32_t i = ln / V, sub = ln % V;
+        return i < m && (int32_t)ent[(size_t)i].size() > t * V + sub;
+      };
+      const int32_t npc = std::max(1, (nsteps + kPieceSteps - 1) / kPieceSteps);
+      if (npc > 255 || nsteps >= 65536) bad |= 4;
+      CsSliceRec Rc{};
+      Rc.p0 = (uint16_t)X.ploc.size();
+      Rc.npieces = (uint8_t)npc;
+      Rc.nsteps = (uint16_t)nsteps;
+      Rc.m = (uint8_t)m;
       for (int32_t k = 0; k < npc; ++k) {
-        const int32_t j0 = k * kPieceSteps, j1 = std::min(maxlen, j0 + kPieceSteps);
+        const int32_t j0 = k * kPieceSteps, j1 = std::min(nsteps, j0 + kPieceSteps);
         int64_t nnzp = 0;
-        for (auto& e : ent) nnzp += std::max(0, std::min((int32_t)e.size(), j1) - j0);
+        for (int32_t t = j0; t < j1; ++t)
+          for (int32_t ln = 0; ln < 32; ++ln) nnzp += valid(ln, t) ? 1 : 0;
         const int64_t bytes = al16((k == 0 ? kSliceMeta : 32) + 10 * nnzp);
         const uint32_t loc = open_piece(bytes);
-        if (k == 0) R.ploc0 = loc;
+        if (k == 0) Rc.ploc0 = loc;
         X.ploc.push_back(loc);
         const size_t at = X.data.size();
         X.data.resize(at + (size_t)bytes, 0);
@@ -323,35 +367,39 @@ int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t w
         uint16_t* eo = reinterpret_cast<uint16_t*>(b);
         int64_t acc = 0;
         for (int32_t u = 0; u < kPieceSteps; ++u) {
-          for (auto& e : ent) acc += ((int32_t)e.size() > j0 + u && j0 + u < j1) ? 1 : 0;
+          if (j0 + u < j1)
+            for (int32_t ln = 0; ln < 32; ++ln) acc += valid(ln, j0 + u) ? 1 : 0;
           eo[u] = (uint16_t)acc;
         }
         b += 32;
-        if (k == 0) {
+        if (k == 0) {  // per lane: its row's window id, length, diagonal
           uint16_t* rid = reinterpret_cast<uint16_t*>(b);
           uint16_t* len = reinterpret_cast<uint16_t*>(b + 64);
           double* dg = reinterpret_cast<double*>(b + 128);
-          for (int32_t u = p; u < q; ++u) {
-            const int32_t r = rows[(size_t)u];
-            rid[u - p] = (uint16_t)(r - r0);
-            len[u - p] = (uint16_t)std::min<int64_t>(offd(r), 65535);
-            dg[u - p] = has_diag(r) ? pv[rp[r]] : 0.0;
+          for (int32_t ln = 0; ln < 32; ++ln) {
+            const int32_t i = ln / V;
+            if (i >= m) continue;
+            const int32_t r = rows[(size_t)(p + i)];
+            rid[ln] = (uint16_t)(r - r0);
+            len[ln] = (uint16_t)std::min<int64_t>(offd(r), 65535);
+            dg[ln] = has_diag(r) ? pv[rp[r]] : 0.0;
           }
           b += kSliceMeta - 32;
         }
         double* val = reinterpret_cast<double*>(b);
         uint16_t* lcol = reinterpret_cast<uint16_t*>(b + 8 * nnzp);
         int64_t e = 0;
-        for (int32_t j = j0; j < j1; ++j)
-          for (int32_t i = 0; i < m; ++i) {
-            if ((int32_t)ent[(size_t)i].size() <= j) break;  // lengths descending
-            val[e] = ent[(size_t)i][(size_t)j].second;
-            lcol[e] = ent[(size_t)i][(size_t)j].first;
-            ++e;
-          }
+        for (int32_t t = j0; t < j1; ++t)
+          for (int32_t ln = 0; ln < 32; ++ln)
+            if (valid(ln, t)) {
+              const Ent& en = ent[(size_t)(ln / V)][(size_t)(t * V + ln % V)];
+              val[e] = en.second;
+              lcol[e] = en.first;
+              ++e;
+            }
         X.nnz += nnzp;
       }
-      X.srec.push_back(R);
+      X.srec.push_back(Rc);
     }
     X.chunk_bytes.push_back(cur);
     if (X.ploc.size() >= 65535) bad |= 2;
@@ -482,7 +530,7 @@ int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t w
           };
           const unsigned char* b0 = piece(R.ploc0);
           const uint16_t* rid = reinterpret_cast<const uint16_t*>(b0 + 32);
-          for (int32_t i = 0; i < R.m; ++i) hit(rid[i]);
+          for (int32_t i = 0; i < R.m; ++i) hit(rid[i * V]);
           for (int32_t k = 0; k < R.npieces; ++k) {
             const unsigned char* b = piece(ploc[R.p0 + k]);
             const int32_t nnzp = reinterpret_cast<const uint16_t*>(b)[15];

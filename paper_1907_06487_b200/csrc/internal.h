@@ -163,7 +163,7 @@ struct CsHost {
 int32_t color_rows_writeset(const int32_t* rp, const int32_t* pc, int32_t r0, int32_t r1,
                             const std::vector<int32_t>& tgt, std::vector<int32_t>& color);
 int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t wcap, int32_t nnzcap,
-                    int32_t chunk_bytes, int32_t stages, CsHost* out);
+                    int32_t chunk_bytes, int32_t stages, int32_t V, CsHost* out);
 
 struct CsArgs {
   const CsDesc* desc;
@@ -175,6 +175,7 @@ struct CsArgs {
   int32_t chunk;                  // bytes of one ring stage
   int32_t stages;                 // ring depth (power of two)
   int32_t lgstages;               // log2(stages)
+  int32_t lgv;                    // log2 of the lanes per row (1, 2 or 4 lanes)
   int32_t debug_skip;             // diagnostics (env SYMM_DEBUG_SKIP): bit0 entries, bit2 flush, bit3 stream only
   unsigned long long* trace;      // diagnostics: CTA 0 event times (nullptr = off), see k_cs
   int32_t trace_cap;              // chunk events [0, cap) x 2, then tile events x 4

@@ -468,19 +468,23 @@ __device__ __forceinline__ void cs_cbar(int nthreads) {
 // shorter are redirected to the zero dummy slot `dummy` with a = 0.  The
 // columns of one row are distinct and rows of one colour are write-disjoint,
 // so all loads of y can precede all stores.
-template <int NU>
+template <int NU, bool V1>
 __device__ __forceinline__ void cs_steps(const double* __restrict__ val, const uint16_t* __restrict__ lc,
-                                         const uint32_t (&ew)[8], int j0, int L, int lane,
+                                         const uint32_t (&ew)[8], int j0, int L, int lgv, int sub, int lane, unsigned lt,
                                          const double* __restrict__ xs, double* ys, double xr, int dummy,
                                          double (&acc)[4]) {
   double a[NU], xv[NU], yv[NU];
   int c[NU];
 #pragma unroll
   for (int u = 0; u < NU; ++u) {
+    // lane (row, sub) holds entry (j0 + u) * V + sub of its row; the valid
+    // lanes of a step are stored in lane order
     const int e0 = u == 0 ? 0 : (int)((ew[(u - 1) >> 1] >> (((u - 1) & 1) * 16)) & 0xffffu);
-    const bool v = L > j0 + u;
-    const double a0 = val[e0 + lane];
-    const int c0 = lc[e0 + lane];
+    const bool v = (((j0 + u) << lgv) + sub) < L;
+    // one lane per row: the valid lanes of a step are a prefix (lengths descend)
+    const int ix = V1 ? e0 + lane : e0 + __popc(__ballot_sync(0xffffffffu, v) & lt);
+    const double a0 = val[ix];
+    const int c0 = lc[ix];
     a[u] = v ? a0 : 0.0;
     c[u] = v ? c0 : dummy;
   }
@@ -635,6 +639,8 @@ CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
         int L = 0, lr = 0;
         double d = 0.0, xr = 0.0;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int sub = lane & ((1 << A.lgv) - 1), row_i = lane >> A.lgv;
+        const unsigned lt = (1u << lane) - 1u;
         CSP(0);
         for (int kp = 0; kp < npc; ++kp) {
           const uint32_t loc = kp == 0 ? ploc0 : ploc[p0 + kp];
@@ -647,7 +653,7 @@ CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
           const uint4 e1 = reinterpret_cast<const uint4*>(b)[1];  // eo[8..15]
           const uint32_t ew[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
           const int nnzp = (int)(e1.w >> 16);
-          if (kp == 0) {  // the slice's rows: window id, length, diagonal (zeros past m)
+          if (kp == 0) {  // the lane's row: window id, length, diagonal (zeros past m)
             lr = reinterpret_cast<const uint16_t*>(b + 32)[lane];
             L = reinterpret_cast<const uint16_t*>(b + 96)[lane];
             d = reinterpret_cast<const double*>(b + 160)[lane];
@@ -660,12 +666,22 @@ CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
           const double* val = reinterpret_cast<const double*>(b);
           const uint16_t* lc = reinterpret_cast<const uint16_t*>(b + 8 * nnzp);
           const int j0 = kp * 16, nst = min(16, nsteps - j0);
-          switch ((nst + 3) >> 2) {
-            case 4: cs_steps<16>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
-            case 3: cs_steps<12>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
-            case 2: cs_steps<8>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
-            case 1: cs_steps<4>(val, lc, ew, j0, L, lane, xsb, ys, xr, Wc, acc); break;
-            default: break;
+          if (A.lgv == 0) {
+            switch ((nst + 3) >> 2) {
+              case 4: cs_steps<16, true>(val, lc, ew, j0, L, 0, 0, lane, lt, xsb, ys, xr, Wc, acc); break;
+              case 3: cs_steps<12, true>(val, lc, ew, j0, L, 0, 0, lane, lt, xsb, ys, xr, Wc, acc); break;
+              case 2: cs_steps<8, true>(val, lc, ew, j0, L, 0, 0, lane, lt, xsb, ys, xr, Wc, acc); break;
+              case 1: cs_steps<4, true>(val, lc, ew, j0, L, 0, 0, lane, lt, xsb, ys, xr, Wc, acc); break;
+              default: break;
+            }
+          } else {
+            switch ((nst + 3) >> 2) {
+              case 4: cs_steps<16, false>(val, lc, ew, j0, L, A.lgv, sub, lane, lt, xsb, ys, xr, Wc, acc); break;
+              case 3: cs_steps<12, false>(val, lc, ew, j0, L, A.lgv, sub, lane, lt, xsb, ys, xr, Wc, acc); break;
+              case 2: cs_steps<8, false>(val, lc, ew, j0, L, A.lgv, sub, lane, lt, xsb, ys, xr, Wc, acc); break;
+              case 1: cs_steps<4, false>(val, lc, ew, j0, L, A.lgv, sub, lane, lt, xsb, ys, xr, Wc, acc); break;
+              default: break;
+            }
           }
           CSP(2);
           __syncwarp();  // every lane is done with the piece: release its share of the stage
@@ -673,7 +689,9 @@ CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
           CSP(3);
           CSP_CNT(8);
         }
-        if (lane < m) ys[lr] += fma(d, xr, (acc[0] + acc[1]) + (acc[2] + acc[3]));
+        double sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        for (int o = (1 << A.lgv) >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (sub == 0 && row_i < m) ys[lr] += fma(d, xr, sum);
         CSP(4);
         CSP_CNT(9);
       }

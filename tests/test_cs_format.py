@@ -28,17 +28,17 @@ assert DESC.itemsize == 64
 RELEASE_UNITS = 4096
 
 
-def dump(s, wcap=4096, chunk=24576, stages=4):
+def dump(s, wcap=4096, chunk=24576, stages=4, V=1):
     f = lib().symm_cs_format_dump
-    f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32] + [C.c_void_p] * 5
+    f.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32] + [C.c_void_p] * 5
     f.restype = C.c_int
     sizes = np.zeros(3, dtype=np.int64)
-    check(f(s._h, wcap, chunk, stages, sizes.ctypes.data, None, None, None, None))
+    check(f(s._h, wcap, chunk, stages, V, sizes.ctypes.data, None, None, None, None))
     desc = np.zeros(int(sizes[0]), dtype=DESC)
     coff = np.zeros(int(sizes[1]), dtype=np.int64)
     clen = np.zeros(int(sizes[1]), dtype=np.int32)
     blocks = np.zeros(int(sizes[2]), dtype=np.uint8)
-    check(f(s._h, wcap, chunk, stages, sizes.ctypes.data, desc.ctypes.data, coff.ctypes.data, clen.ctypes.data,
+    check(f(s._h, wcap, chunk, stages, V, sizes.ctypes.data, desc.ctypes.data, coff.ctypes.data, clen.ctypes.data,
             blocks.ctypes.data))
     return desc, coff, clen, blocks
 
@@ -47,7 +47,7 @@ def u16(b, off, n):
     return np.frombuffer(b, dtype="<u2", count=n, offset=off)
 
 
-def decode_and_multiply(desc, coff, clen, blocks, n, xp):
+def decode_and_multiply(desc, coff, clen, blocks, n, xp, V=1):
     """y = A x from the K5 blocks, walked like k_cs; also returns the set of
     (row, col) pairs the blocks encode (global permuted ids) for coverage."""
     b = blocks.tobytes()
@@ -82,12 +82,13 @@ def decode_and_multiply(desc, coff, clen, blocks, n, xp):
             for s in range(int(cslc[kk]), int(cslc[kk + 1])):
                 ploc0, w1, w2, _ = (int(v) for v in srec[s])
                 p0, nsteps, npc, m = w1 & 0xFFFF, w1 >> 16, w2 & 0xFF, (w2 >> 8) & 0xFF
-                assert int(ploc[p0]) == ploc0 and 1 <= m <= 32
+                assert int(ploc[p0]) == ploc0 and 1 <= m <= 32 // V
                 o = piece(ploc0)
-                rid = u16(b, o + 32, 32)[:m].astype(np.int64)
-                L = u16(b, o + 96, 32)[:m].astype(np.int64)
-                d = np.frombuffer(b, dtype="<f8", count=32, offset=o + 160)[:m]
-                assert np.all(np.diff(L) <= 0) and int(L[0]) == nsteps  # lengths descend
+                lane_rid = u16(b, o + 32, 32).astype(np.int64)
+                lane_L = u16(b, o + 96, 32).astype(np.int64)
+                lane_d = np.frombuffer(b, dtype="<f8", count=32, offset=o + 160)
+                rid, L, d = lane_rid[::V][:m], lane_L[::V][:m], lane_d[::V][:m]
+                assert np.all(np.diff(L) <= 0) and (int(L[0]) + V - 1) // V == nsteps  # lengths descend
                 acc = d * xs[rid]
                 for r in rid:  # a row's own slot is in its colour's write set
                     assert int(r) not in written
@@ -100,12 +101,13 @@ def decode_and_multiply(desc, coff, clen, blocks, n, xp):
                     val = np.frombuffer(b, dtype="<f8", count=nnzp, offset=vo)
                     lc = u16(b, vo + 8 * nnzp, nnzp).astype(np.int64)
                     for u in range(16):
-                        j = 16 * kp + u
+                        t = 16 * kp + u
                         start = 0 if u == 0 else int(eo[u - 1])
-                        lanes = np.nonzero(L > j)[0]
+                        lanes = [ln for ln in range(32) if ln // V < m and L[ln // V] > t * V + ln % V]
                         assert int(eo[u]) - start == len(lanes)
-                        for i in lanes:  # JDS: lane i's entry at step j is start + i
-                            a, c = val[start + i], int(lc[start + i])
+                        for rank, ln in enumerate(lanes):  # JDS: rank among the step's valid lanes
+                            i = ln // V
+                            a, c = val[start + rank], int(lc[start + rank])
                             assert c not in written  # write-disjoint colour
                             written.add(c)
                             acc[i] += a * xs[c]           # tmp += A[idx] x[col]
@@ -118,18 +120,18 @@ def decode_and_multiply(desc, coff, clen, blocks, n, xp):
 
 
 @pytest.mark.parametrize("name", ["lap2d_64", "st27_24", "spin_14", "fem_knn_30k"])
-@pytest.mark.parametrize("wcap", [512, 4096])
-def test_cs_format_decodes_to_oracle(name, wcap):
+@pytest.mark.parametrize("wcap,V", [(512, 1), (4096, 1), (4096, 2), (2048, 4)])
+def test_cs_format_decodes_to_oracle(name, wcap, V):
     U, x = gen.make_config(name)
-    if U.n > 20000 and wcap == 512:
+    if U.n > 20000 and (wcap, V) != (4096, 1):
         pytest.skip("python decode time")
     s = P.build_schedule(U)
     perm, inv = s.permutation()
-    desc, coff, clen, blocks = dump(s, wcap=wcap)
+    desc, coff, clen, blocks = dump(s, wcap=wcap, V=V)
     assert int(desc["T"].sum()) == U.n                      # tiles partition the rows
     assert np.array_equal(np.cumsum(desc["T"])[:-1], desc["row0"][1:])
     xp = x[inv]
-    y, pairs = decode_and_multiply(desc, coff, clen, blocks, U.n, xp)
+    y, pairs = decode_and_multiply(desc, coff, clen, blocks, U.n, xp, V)
     y_ref = oracle.symmspmv(U, x)
     err = np.max(np.abs(y[perm] - y_ref)) / np.max(np.abs(y_ref))
     assert err <= 1e-13, err
