@@ -16,6 +16,8 @@ pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
 VARIANTS = ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem")
+# fp64 RED flushes: run-to-run summation order varies (reading R5)
+NONDET = ("atomic", "tiled_atomic", "colored_smem")
 
 
 def _torch():
@@ -57,7 +59,7 @@ SMALL = ["lap2d_64", "st27_24", "fem_knn_30k", "spin_14", "lap3d_40"]
 def test_parity_small_configs(name, variant):
     U, x = gen.make_config(name)
     y_ref = oracle.symmspmv(U, x)
-    outs, plan, _ = run_gpu(U, x, variant, repeats=3 if "atomic" not in variant else 1)
+    outs, plan, _ = run_gpu(U, x, variant, repeats=3 if variant not in NONDET else 1)
     assert relinf(outs[0], y_ref) <= TOL
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])  # colored/tiled: bitwise deterministic
@@ -103,7 +105,7 @@ def test_many_tiles_small_windows(variant):
     outs, _, s = run_gpu(U, x, variant, sched_kw=dict(tile_work=200, max_tile_window=512), repeats=3)
     assert s.stats["n_tiles"] > 300
     assert relinf(outs[0], oracle.symmspmv(U, x)) <= TOL
-    if "atomic" not in variant:
+    if variant not in NONDET:
         assert all(np.array_equal(o, outs[0]) for o in outs)
 
 
