@@ -161,11 +161,66 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     for (int32_t r = S.tile_ptr[(size_t)t]; r < S.tile_ptr[(size_t)t + 1]; ++r) tile_of[(size_t)r] = t;
   std::vector<TileDesc> desc((size_t)nt);
   std::vector<int64_t> boff((size_t)nt + 1, 0);
+  // spill windows laid out run by run: a run of consecutive target rows g..
+  // starts on a window id w with w == g - row0 (mod 2), so that with the
+  // window shifted like the own rows (slot parity == row parity) a run can
+  // be bulk-copied from x; a pad slot (target -1) fixes the parity
+  std::vector<int64_t> slot_ptr((size_t)nt + 1, 0), run_ptr((size_t)nt + 1, 0);
+  // runs averaging >= 6 targets are bulk-copied by the gather warps (measured:
+  // st27, spin, lap3d); shorter runs (kNN) are gathered slot by slot and need
+  // no parity pads
+  std::vector<char> use_runs((size_t)nt, 0);
+  for (int32_t t = 0; t < nt; ++t) {
+    int64_t nr = 0;
+    int32_t prev = -2;
+    for (int64_t q = S.spill_ptr[(size_t)t]; q < S.spill_ptr[(size_t)t + 1]; ++q) {
+      const int32_t g = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
+      nr += (g != prev + 1);
+      prev = g;
+    }
+    use_runs[(size_t)t] = nr > 0 && (S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]) >= 6 * nr;
+  }
+  for (int32_t t = 0; t < nt; ++t) {
+    const int32_t r0 = S.tile_ptr[(size_t)t], T = S.tile_ptr[(size_t)t + 1] - r0;
+    int64_t w = 0, nr = 0;
+    int32_t prev = -2;
+    for (int64_t q = S.spill_ptr[(size_t)t]; q < S.spill_ptr[(size_t)t + 1]; ++q) {
+      const int32_t g = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
+      if (g != prev + 1) {
+        ++nr;
+        if (use_runs[(size_t)t] && ((T + w - (g - r0)) & 1) != 0) ++w;  // window id T + w == g - row0 (mod 2)
+      }
+      ++w;
+      prev = g;
+    }
+    slot_ptr[(size_t)t + 1] = slot_ptr[(size_t)t] + w;
+    run_ptr[(size_t)t + 1] = run_ptr[(size_t)t] + nr;
+  }
+  std::vector<int32_t> slot_tgt((size_t)slot_ptr[(size_t)nt], -1);
+
+  std::vector<SpillRun> runs((size_t)run_ptr[(size_t)nt]);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int32_t t = 0; t < nt; ++t) {
+    const int32_t r0 = S.tile_ptr[(size_t)t], T = S.tile_ptr[(size_t)t + 1] - r0;
+    int64_t w = 0, nr = run_ptr[(size_t)t];
+    int32_t prev = -2;
+    for (int64_t q = S.spill_ptr[(size_t)t]; q < S.spill_ptr[(size_t)t + 1]; ++q) {
+      const int32_t g = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
+      if (g != prev + 1) {
+        if (use_runs[(size_t)t] && ((T + w - (g - r0)) & 1) != 0) ++w;
+        runs[(size_t)nr++] = SpillRun{g, T + (int32_t)w, 0, 0};
+      }
+      runs[(size_t)nr - 1].len++;
+      slot_tgt[(size_t)(slot_ptr[(size_t)t] + w)] = g;
+      ++w;
+      prev = g;
+    }
+  }
   int32_t block_cap = 16, window_cap = 2, nnz_cap = 2;
   int bad = 0;
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
-    const int32_t S_ = (int32_t)(S.spill_ptr[(size_t)t + 1] - S.spill_ptr[(size_t)t]);
+    const int32_t S_ = (int32_t)(slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
     const int64_t nnz = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
     int32_t nd = 0;
     for (int32_t r = r0; r < r1; ++r)
@@ -193,7 +248,10 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     D.o_tgt = (uint16_t)o_tgt;
     D.o_slot = (uint16_t)o_slot;
     D.o_val = (uint16_t)o_val;
-    D.spill_off = (int32_t)S.spill_ptr[(size_t)t];
+    D.spill_off = (int32_t)slot_ptr[(size_t)t];
+    D.run_off = (int32_t)run_ptr[(size_t)t];
+    D.nruns = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
+    D.gather_runs = use_runs[(size_t)t];
     boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
     D.block_off = boff[(size_t)t];
     block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
@@ -204,22 +262,25 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     return set_error(SYMM_ERR_UNSUPPORTED, "tile %d does not fit the 64 KB tile-block format (use smaller tiles)", bad - 1);
   window_cap = (window_cap + 2 + 15) & ~15;  // +2: x window alignment shift; stages stay 128-B aligned
   block_cap = (block_cap + 127) & ~127;
-  // staged contributions: slot order = (owner row, writer tile, ...) -> contiguous per row
-  const int64_t nsp = (int64_t)S.spill.size();
-  std::vector<int32_t> in_ptr((size_t)n + 1, 0), slots((size_t)nsp);
-  for (int64_t q = 0; q < nsp; ++q) in_ptr[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask) + 1]++;
+  // staged contributions (K3): one staging slot per (writer tile, target);
+  // slot order = (owner row, writer tile) -> contiguous per row
+  const int64_t nsl = slot_ptr[(size_t)nt];
+  std::vector<int32_t> in_ptr((size_t)n + 1, 0), slots((size_t)nsl, -1);
+  for (int64_t q = 0; q < nsl; ++q)
+    if (slot_tgt[(size_t)q] >= 0) in_ptr[(size_t)slot_tgt[(size_t)q] + 1]++;
   for (int32_t r = 0; r < n; ++r) in_ptr[(size_t)r + 1] += in_ptr[(size_t)r];
+  const int64_t nsp = in_ptr[(size_t)n];
   {
     std::vector<int32_t> pos(in_ptr.begin(), in_ptr.end() - 1);
-    for (int64_t q = 0; q < nsp; ++q)  // ascending writer tile, then ascending target
-      slots[(size_t)q] = pos[(size_t)((uint32_t)S.spill[(size_t)q] & kIdxMask)]++;
+    for (int64_t q = 0; q < nsl; ++q)  // ascending writer tile, then ascending target
+      if (slot_tgt[(size_t)q] >= 0) slots[(size_t)q] = pos[(size_t)slot_tgt[(size_t)q]]++;
   }
   std::vector<unsigned char> blocks((size_t)boff[(size_t)nt], 0);
 #pragma omp parallel for schedule(dynamic, 8) reduction(| : bad)
   for (int32_t t = 0; t < nt; ++t) {
     const TileDesc& D = desc[(size_t)t];
     const int32_t r0 = D.row0, T = D.nrows, r1 = r0 + T, ns = D.nspill, W = T + ns;
-    const int32_t* sp = S.spill.data() + S.spill_ptr[(size_t)t];
+    const int32_t* st = slot_tgt.data() + slot_ptr[(size_t)t];
     unsigned char* blk = blocks.data() + D.block_off;
     std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
     uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
@@ -228,43 +289,92 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
-    for (int32_t j = 0; j < ns; ++j) tgt[j] = (int32_t)((uint32_t)sp[j] & kIdxMask);
+    for (int32_t j = 0; j < ns; ++j) tgt[j] = st[j];  // flush target of every spill slot (-1 = pad)
     const int32_t e0 = S.prow_ptr[(size_t)r0];
-    std::vector<int32_t> tcnt((size_t)W + 1, 0);
-    for (int32_t r = r0; r < r1; ++r) {
-      start[r - r0] = (uint16_t)(S.prow_ptr[(size_t)r] - e0);
-      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
-        const int32_t c = S.pcol[(size_t)i];
-        int32_t l;
-        if (c < r1) l = c - r0;
-        else {
-          int32_t lo = 0, hi = ns;
-          while (lo < hi) {
-            int32_t mid = (lo + hi) / 2;
-            if (tgt[mid] < c) lo = mid + 1;
-            else hi = mid;
-          }
-          if (lo >= ns || tgt[lo] != c) bad |= 1;
-          l = T + lo;
+    // window id of a target: own rows 0..T-1; spill targets through the runs
+    const SpillRun* tr = runs.data() + run_ptr[(size_t)t];
+    const int32_t nrt = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
+    auto local = [&](int32_t c) -> int32_t {
+      if (c < r1) return c - r0;
+      int32_t lo = 0, hi = nrt;  // last run with first row <= c
+      while (lo < hi) {
+        int32_t mid = (lo + hi) / 2;
+        if (tr[mid].row <= c) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo == 0 || c >= tr[lo - 1].row + tr[lo - 1].len) {
+        bad |= 1;
+        return 0;
+      }
+      return tr[lo - 1].wid + (c - tr[lo - 1].row);
+    };
+    // row pass: the 32 consecutive rows of a warp are walked in lock step;
+    // order every row's entries so that at each step the x gathers of a half
+    // warp hit distinct bank pairs (window id mod 16)
+    std::vector<std::vector<std::pair<uint16_t, double>>> ent;
+    for (int32_t w0 = 0; w0 < T; w0 += 32) {
+      const int32_t w1 = std::min(T, w0 + 32);
+      ent.assign((size_t)(w1 - w0), {});
+      for (int32_t r = r0 + w0; r < r0 + w1; ++r)
+        for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
+          ent[(size_t)(r - r0 - w0)].push_back({(uint16_t)local(S.pcol[(size_t)i]), S.pval[(size_t)i]});
+      if (!std::getenv("SYMM_NO_BANK_ORDER")) bank_order_rows(ent, 1);
+      for (int32_t r = r0 + w0; r < r0 + w1; ++r) {
+        const auto& e = ent[(size_t)(r - r0 - w0)];
+        const int32_t b = S.prow_ptr[(size_t)r] - e0;
+        start[r - r0] = (uint16_t)b;
+        for (size_t k = 0; k < e.size(); ++k) {
+          lcol[b + (int32_t)k] = e[k].first;
+          val[b + (int32_t)k] = e[k].second;
         }
-        lcol[i - e0] = (uint16_t)l;
-        val[i - e0] = S.pval[(size_t)i];
-        if (c != r) tcnt[(size_t)l + 1]++;
       }
     }
     start[T] = (uint16_t)(S.prow_ptr[(size_t)r1] - e0);
-    for (int32_t l = 0; l < W; ++l) tcnt[(size_t)l + 1] += tcnt[(size_t)l];
-    for (int32_t l = 0; l <= W; ++l) tptr[l] = (uint16_t)tcnt[(size_t)l];
+    // CSC pass: target l's list of (entry, local row); at each step the lanes
+    // of a half warp (32 consecutive targets) should read val[entry] and
+    // xs[row] from distinct bank pairs
+    std::vector<std::vector<uint32_t>> lists((size_t)W);
     for (int32_t r = r0; r < r1; ++r)
-      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
-        if (S.pcol[(size_t)i] != r) tcsc[tcnt[lcol[i - e0]]++] = (uint32_t)(i - e0) | ((uint32_t)(r - r0) << 16);
+      for (int32_t k = start[r - r0]; k < start[r - r0 + 1]; ++k)
+        if (lcol[k] != r - r0) lists[lcol[k]].push_back((uint32_t)k | ((uint32_t)(r - r0) << 16));
+    const int32_t vb = (int32_t)(D.o_val / 8);  // bank-pair phase of val[0]
+    if (!std::getenv("SYMM_NO_BANK_ORDER"))
+      for (int32_t w0 = 0; w0 < W; w0 += 32) {
+        const int32_t w1 = std::min(W, w0 + 32);
+        size_t maxlen = 0;
+        for (int32_t l = w0; l < w1; ++l) maxlen = std::max(maxlen, lists[(size_t)l].size());
+        for (size_t j = 0; j < maxlen; ++j)
+          for (int32_t h = w0; h < w1; h += 16) {
+            uint32_t usedv = 0, usedr = 0;
+            for (int32_t l = h; l < std::min(w1, h + 16); ++l) {
+              auto& L = lists[(size_t)l];
+              if (L.size() <= j) continue;
+              size_t best = j;
+              int bestscore = -1;
+              for (size_t q = j; q < L.size(); ++q) {
+                const uint32_t bv = (uint32_t)(((L[q] & 0xffffu) + vb) & 15), br = (L[q] >> 16) & 15;
+                const int sc = (((usedv >> bv) & 1) ? 0 : 2) + (((usedr >> br) & 1) ? 0 : 1);
+                if (sc > bestscore) { bestscore = sc; best = q; if (sc == 3) break; }
+              }
+              std::swap(L[j], L[best]);
+              usedv |= 1u << (((L[j] & 0xffffu) + vb) & 15);
+              usedr |= 1u << ((L[j] >> 16) & 15);
+            }
+          }
+      }
+    int32_t pos = 0;
+    for (int32_t l = 0; l < W; ++l) {
+      tptr[l] = (uint16_t)pos;
+      for (uint32_t q : lists[(size_t)l]) tcsc[pos++] = q;
+    }
+    tptr[W] = (uint16_t)pos;
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   // multi-rank: keep only this rank's tiles (descriptors re-based to the range)
   if (t_begin != 0 || t_end != nt) {
     const int64_t b0 = boff[(size_t)t_begin], b1 = boff[(size_t)t_end];
     std::vector<TileDesc> d2(desc.begin() + t_begin, desc.begin() + t_end);
-    for (auto& D : d2) D.block_off -= b0;
+    for (auto& D : d2) D.block_off -= b0;  // runs / targets / slots stay global arrays
     std::vector<unsigned char> bl2(blocks.begin() + b0, blocks.begin() + b1);
     for (size_t i = 0; i < d2.size(); ++i)
       std::memcpy(bl2.data() + d2[i].block_off, &d2[i], sizeof(TileDesc));
@@ -276,13 +386,12 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   unsigned char* d_blocks;
   double* d_spill;
   int32_t *d_targets, *d_slots;
-  std::vector<int32_t> targets((size_t)nsp);
-  for (int64_t q = 0; q < nsp; ++q) targets[(size_t)q] = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
+  SpillRun* d_runs;
   int rc;
   if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
-      (rc = upload(P, &d_targets, targets.data(), targets.size())) ||
-      (rc = upload(P, &d_slots, slots.data(), slots.size())) ||
-      (rc = upload(P, &P->d_in_ptr, in_ptr.data(), in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)nsp)))
+      (rc = upload(P, &d_targets, slot_tgt.data(), slot_tgt.size())) ||
+      (rc = upload(P, &d_slots, slots.data(), slots.size())) || (rc = upload(P, &d_runs, runs.data(), runs.size())) ||
+      (rc = upload(P, &P->d_in_ptr, in_ptr.data(), in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
     return rc;
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
@@ -290,6 +399,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   A.blocks = d_blocks;
   A.targets = d_targets;
   A.slots = d_slots;
+  A.runs = d_runs;
   A.spill_buf = d_spill;
   A.block_cap = block_cap;
   A.window_cap = window_cap;

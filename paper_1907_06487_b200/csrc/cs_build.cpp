@@ -191,6 +191,8 @@ int64_t bank_order(std::vector<std::vector<Ent>>& ent, int V) {
 
 }  // namespace
 
+int64_t bank_order_rows(std::vector<std::vector<std::pair<uint16_t, double>>>& ent, int V) { return bank_order(ent, V); }
+
 int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t wcap, int32_t nnzcap,
                     int32_t chunk_bytes, int32_t stages, int32_t V, CsHost* out) {
   if (V != 1 && V != 2 && V != 4) return set_error(SYMM_ERR_ARG, "lanes per row %d (1, 2 or 4)", V);

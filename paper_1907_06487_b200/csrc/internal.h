@@ -79,21 +79,33 @@ struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
   int32_t nrows;        // T
-  int32_t nspill;       // S (window W = T + S)
+  int32_t nspill;       // S = spill window slots (window W = T + S): the spill targets
+                        // laid out run by run, a run of consecutive rows starting on a slot
+                        // of the same 16-B parity as its first row (bulk-copyable); pad slots
+                        // have target -1
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
   uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block (o_slot unused)
-  int32_t spill_off;    // first spill entry of this tile (targets / slots arrays)
-  int32_t pad[5];
+  int32_t spill_off;    // first spill slot of this tile (targets / slots arrays)
+  int32_t run_off;      // first run of this tile (runs array)
+  int32_t nruns;        // runs of consecutive spill targets
+  int32_t gather_runs;  // 1: the gather warps bulk-copy the runs (long runs); 0: they
+                        // cp.async slot by slot from the block's tgt list (short runs)
+  int32_t pad[2];
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
+
+struct SpillRun {                 // consecutive spill targets row .. row+len-1 at window ids wid..
+  int32_t row, wid, len, pad;
+};
 
 struct TiledArgs {
   const TileDesc* tiles;          // tile id order (= BFS order)
   int32_t ntiles;
   const unsigned char* blocks;
-  const int32_t* targets;         // spill targets of all tiles (tile order)
-  const int32_t* slots;           // K3: staging slot of every spill entry (tile order)
+  const int32_t* targets;         // spill target of every spill slot of all tiles (-1 = pad)
+  const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)
+  const struct SpillRun* runs;    // every spill run of every tile (tile order)
   double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)
@@ -160,6 +172,10 @@ struct CsHost {
   int32_t Wcap = 16, Hcap = 16, max_colour_chunks = 1;
   int64_t nnz_offdiag = 0, sum_colors = 0, sum_slices = 0, sum_spill = 0, conflicts = 0, steps = 0;
 };
+// Bank-aware step order of the rows of one warp (cs_build.cpp): entry lists
+// (window id, value) reordered so that at each step the lanes of a half warp
+// address distinct shared-memory bank pairs (window id mod 16).
+int64_t bank_order_rows(std::vector<std::vector<std::pair<uint16_t, double>>>& ent, int V);
 int32_t color_rows_writeset(const int32_t* rp, const int32_t* pc, int32_t r0, int32_t r1,
                             const std::vector<int32_t>& tgt, std::vector<int32_t>& color);
 int build_cs_format(const Schedule& S, int32_t t_begin, int32_t t_end, int32_t wcap, int32_t nnzcap,

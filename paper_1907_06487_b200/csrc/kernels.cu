@@ -188,6 +188,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
   asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -322,26 +325,68 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   }
   if (wid >= kGroups * kGroupWarps + 1) {
     // ------------------------------------------------ gather warps (x window)
-    // kGatherWarps warps take the tiles of this CTA in turn; each waits for its
-    // tile's block (the loader runs ahead), then cp.async-gathers the spill
-    // targets (read from shared memory) and the unaligned own-x edge elements.
+    // kGatherWarps warps take the tiles of this CTA in turn.  As soon as the
+    // stage is free (no need to wait for the tile's block) a warp fills the
+    // spill part of the x window: the spill targets come as runs of
+    // consecutive rows laid out with matching 16-B parity, so each run is one
+    // bulk copy (TMA) plus at most two 8-B cp.async edge elements; the lane also
+    // copies the unaligned own-x edge elements (the loader bulk-copies the rest).
     const int gw = wid - (kGroups * kGroupWarps + 1);
     int k = gw;
     for (int t = blockIdx.x + gw * G; t < A.ntiles; t += kGatherWarps * G, k += kGatherWarps) {
       const int s = k % NS;
-      mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));
+      const TileDesc* Dg = A.tiles + t;
+      const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
+      const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
+      if (k >= NS) mbar_wait(&empty[s], (unsigned)(((k / NS) - 1) & 1));  // stage free
       if (lane == 0) TRACE(k, 1);
-      const unsigned char* blk = sm + s * slot_bytes;
-      const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
-      const int row0 = D.row0, T = D.nrows, S = D.nspill;
-      const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
       const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
       const int nfull = T > p ? ((T - p) & ~1) : 0;
       double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
       if (lane == 0 && p == 1) cp_async8(xs, x + row0);
       if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
+      if (A.debug_skip & 8) {
+        // diagnostics: no spill gather
+      } else if (__ldg(&Dg->gather_runs)) {
+        // long runs: as soon as the stage is free, one bulk copy per run (+ <= 2
+        // 8-B edge elements); run records of this tile, 8 per lane per batch,
+        // are loaded before any copy is issued
+        for (int rb = 0; rb < nr; rb += 32 * 8) {
+          int4 R[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = rb + u * 32 + lane;
+            R[u] = r < nr ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int len = R[u].z;  // (row, wid, len, 0)
+            if (len <= 0) continue;
+            double* dst = xs + R[u].y;
+            const double* src = x + R[u].x;
+            const int i0 = (int)(((uintptr_t)src >> 3) & 1);  // dst has the same 16-B phase
+            const int nb = len > i0 ? ((len - i0) & ~1) : 0;
+            if (nb > 0) {
+              mbar_expect_tx(&x_full[s], (unsigned)nb * 8u);
+              bulk_g2s(dst + i0, src + i0, (unsigned)nb * 8u, &x_full[s]);
+            }
+            if (i0) cp_async8(dst, src);
+            if (i0 + nb < len) cp_async8(dst + len - 1, src + len - 1);
+          }
+        }
+      } else {
+        // short runs: slot by slot from the block's target list, spread over the lanes
+        mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));
+        const unsigned char* blk = sm + s * slot_bytes;
+        const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
+        const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
+        const int S = D.nspill;
 #pragma unroll 4
-      for (int idx = lane; idx < S && !(A.debug_skip & 8); idx += 32) cp_async8(xs + T + idx, x + tgt[idx]);
+        for (int idx = lane; idx < S; idx += 32) {
+          const int g = tgt[idx];
+          if (g >= 0) cp_async8(xs + T + idx, x + g);
+        }
+      }
       cp_async_arrive_noinc(&x_full[s]);
       if (lane == 0) TRACE(k, 2);
     }
@@ -388,10 +433,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       if (A.debug_skip & 4) {
         // diagnostics: no flush
       } else if (ATOMIC) {
-        atomicAdd(y + (l < T ? row0 + l : tgt[l - T]), acc);
+        const int gr = l < T ? row0 + l : tgt[l - T];
+        if (gr >= 0) atomicAdd(y + gr, acc);  // -1: pad slot of the spill window
       } else if (l < T) {
         y[row0 + l] = acc;
-      } else {
+      } else if (sl >= 0) {
         __stcg(A.spill_buf + sl, acc);
       }
     }
