@@ -173,7 +173,7 @@ constexpr int kMaxStages = 8;
 constexpr int kGroupWarps = 6;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 4;
-constexpr int kGatherWarps = 2;
+constexpr int kGatherWarps = 4;
 constexpr int kTiledThreads = kGroups * kGroupThreads + 32 * (1 + kGatherWarps);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
                                                             double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t blk_full[NS], x_full[NS], empty[NS];
+  __shared__ int loader_k;  // tiles the loader has taken a free stage for (gather warps follow it)
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       mbar_init(&empty[s], kGroupWarps);  // every consumer warp of the group arrives
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    loader_k = 0;
   }
   __syncthreads();
   if (wid == kGroups * kGroupWarps) {
@@ -296,6 +298,8 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         TRACE(k, 6);
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
         TRACE(k, 7);
+        // the stage of tile k is free: gather warps may fill its x window
+        asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(smem_u32(&loader_k)), "r"(k + 1) : "memory");
         double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
         mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z + xbytes);
         bulk_g2s_stream(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s], pol);
@@ -338,7 +342,23 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       const TileDesc* Dg = A.tiles + t;
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
       const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
-      if (k >= NS) mbar_wait(&empty[s], (unsigned)(((k / NS) - 1) & 1));  // stage free
+      const int gruns = __ldg(&Dg->gather_runs) && !(A.debug_skip & 8);
+      // the first batch of run records (8 per lane) is loaded before the stage
+      // wait, so its latency overlaps it
+      int4 R[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = u * 32 + lane;
+        R[u] = (gruns && r < nr) ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
+      }
+      // stage free: the loader (which waits for the stages in order, so its
+      // parity waits cannot alias) has passed tile k
+      while (true) {
+        int lk;
+        asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(lk) : "r"(smem_u32(&loader_k)) : "memory");
+        if (lk > k) break;
+        __nanosleep(32);
+      }
       if (lane == 0) TRACE(k, 1);
       const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
       const int nfull = T > p ? ((T - p) & ~1) : 0;
@@ -347,16 +367,15 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
       if (A.debug_skip & 8) {
         // diagnostics: no spill gather
-      } else if (__ldg(&Dg->gather_runs)) {
-        // long runs: as soon as the stage is free, one bulk copy per run (+ <= 2
-        // 8-B edge elements); run records of this tile, 8 per lane per batch,
-        // are loaded before any copy is issued
+      } else if (gruns) {
+        // long runs: one bulk copy per run (+ <= 2 8-B edge elements)
         for (int rb = 0; rb < nr; rb += 32 * 8) {
-          int4 R[8];
+          if (rb > 0) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int r = rb + u * 32 + lane;
-            R[u] = r < nr ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
+            for (int u = 0; u < 8; ++u) {
+              const int r = rb + u * 32 + lane;
+              R[u] = r < nr ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
+            }
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
