@@ -170,10 +170,10 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
 constexpr int kMaxStages = 8;
-constexpr int kGroupWarps = 6;
+constexpr int kGroupWarps = 7;
 constexpr int kGroupThreads = kGroupWarps * 32;
 constexpr int kGroups = 4;
-constexpr int kGatherWarps = 4;
+constexpr int kGatherWarps = 3;
 constexpr int kTiledThreads = kGroups * kGroupThreads + 32 * (1 + kGatherWarps);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
