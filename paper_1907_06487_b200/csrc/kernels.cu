@@ -51,6 +51,9 @@ __device__ __forceinline__ double group_sum(double s) {
 
 // ---------------------------------------------------------------- zero / gather
 __global__ void k_zero(double* __restrict__ y, int64_t n) {
+  // the tiled kernel that follows may start streaming its (constant) tile
+  // blocks now; it waits (griddepcontrol.wait) before touching x or y
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // 16-B stores for the aligned body, scalar head/tail
   const int64_t head = ((16 - ((uintptr_t)y & 15)) & 15) / 8;  // 0 or 1 element
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -290,20 +293,17 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int s = k % NS, use = k / NS;
         const int64_t off = (int64_t)(uint32_t)d.x | ((int64_t)d.y << 32);
         const int row0 = d.w;
-        // 16-B aligned part of x[row0 .. row0+T) by TMA too; the gather warps
-        // add the (at most two) unaligned edge elements and the spill targets
-        const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
-        const int nfull = T > p ? ((T - p) & ~1) : 0;
-        const unsigned xbytes = (unsigned)nfull * 8u;
+        (void)row0;
+        (void)T;
         TRACE(k, 6);
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
         TRACE(k, 7);
         // the stage of tile k is free: gather warps may fill its x window
         asm volatile("st.volatile.shared.s32 [%0], %1;" ::"r"(smem_u32(&loader_k)), "r"(k + 1) : "memory");
-        double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
-        mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z + xbytes);
+        // the loader reads only the plan's tile blocks (never x or y), so it
+        // may run while the preceding kernel (k_zero) still runs (PDL)
+        mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z);
         bulk_g2s_stream(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s], pol);
-        if (xbytes) bulk_g2s(xs + p, x + row0 + p, xbytes, &blk_full[s]);
         TRACE(k, 0);
       };
       ld(0, d0, T0);
@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // bulk copy (TMA) plus at most two 8-B cp.async edge elements; the lane also
     // copies the unaligned own-x edge elements (the loader bulk-copies the rest).
     const int gw = wid - (kGroups * kGroupWarps + 1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // x is ready (PDL prerequisite done)
     int k = gw;
     for (int t = blockIdx.x + gw * G; t < A.ntiles; t += kGatherWarps * G, k += kGatherWarps) {
       const int s = k % NS;
@@ -363,6 +364,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
       const int nfull = T > p ? ((T - p) & ~1) : 0;
       double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
+      // own rows: the 16-B aligned part of x[row0 .. row0+T) by one bulk copy,
+      // the (at most two) unaligned edge elements by cp.async
+      if (lane == 2 && nfull > 0) {
+        mbar_expect_tx(&x_full[s], (unsigned)nfull * 8u);
+        bulk_g2s(xs + p, x + row0 + p, (unsigned)nfull * 8u, &x_full[s]);
+      }
       if (lane == 0 && p == 1) cp_async8(xs, x + row0);
       if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
       if (A.debug_skip & 8) {
@@ -412,6 +419,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     return;
   }
   // -------------------------------------------------- consumer groups
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // y is zeroed (PDL prerequisite done)
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
   int k = g;
@@ -890,21 +898,33 @@ int tiled_max_ctas_per_sm(int vec, const TiledArgs& T0, int* out) {
 int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream) {
   (void)vec;
   if (T.ntiles <= 0) return 0;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int smem = tiled_smem_bytes(T);
-#define LT(NSV)                                                                             \
-  case NSV:                                                                                 \
-    if (atomic_flush) k_tiled<true, NSV><<<grid, kTiledThreads, smem, st>>>(T, x, y);       \
-    else k_tiled<false, NSV><<<grid, kTiledThreads, smem, st>>>(T, x, y);                   \
+  // programmatic dependent launch: the kernel's loader streams tile blocks
+  // while the previous kernel of the stream finishes; every access to x or y
+  // waits for it (griddepcontrol.wait)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kTiledThreads);
+  cfg.dynamicSmemBytes = (size_t)tiled_smem_bytes(T);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaErrorInvalidValue;
+#define LT(NSV)                                                                 \
+  case NSV:                                                                     \
+    e = atomic_flush ? cudaLaunchKernelEx(&cfg, k_tiled<true, NSV>, T, x, y)    \
+                     : cudaLaunchKernelEx(&cfg, k_tiled<false, NSV>, T, x, y);  \
     break;
   switch (T.stages) {
     LT(8) LT(6) LT(5) LT(4) LT(3) LT(2)
     default: return (int)cudaErrorInvalidValue;
   }
 #undef LT
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
-
 
 int cs_smem_bytes(const CsArgs& A) {
   const int64_t Hb = (A.Hcap + 127) & ~127, Ws = ((A.Wcap + 15) & ~15) + 16;

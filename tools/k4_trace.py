@@ -19,9 +19,10 @@ torch.cuda.synchronize()
 L = C.CDLL(_lib.LIB_PATH)
 L.symmspmv_debug_trace.argtypes = [C.c_void_p] * 5 + [C.c_int32]
 cap = 4096
-tr = np.zeros(cap * 8, dtype=np.uint64)
+tr = np.zeros(cap * 8 + 16, dtype=np.uint64)
 assert L.symmspmv_debug_trace(plan._h, C.c_void_p(xd.data_ptr()), C.c_void_p(yd.data_ptr()), None, tr.ctypes.data, cap) == 0
-tr = tr.reshape(cap, 8).astype(np.int64)
+prof = tr[cap * 8: cap * 8 + 6].astype(np.float64)
+tr = tr[:cap * 8].reshape(cap, 8).astype(np.int64)
 n = int(np.count_nonzero(tr[:, 5])); tr = tr[:n]; t0 = tr[:, 6].min()
 print("plan", plan.info(), "tiles of CTA0:", n, "span us", (tr[:, 5].max() - t0) / 1e3)
 for nm, (a, b) in {"loader empty-wait": (6, 7), "loader issue": (7, 0), "gather issue (1->2)": (1, 2),
@@ -33,3 +34,7 @@ c3 = np.sort(tr[:, 3]); c4 = np.sort(tr[:, 4])
 print("consumer start interval median (4 groups interleaved):", np.median(np.diff(c3)))
 for i in range(8, 20):
     print(i, [int((v - t0) / 10) / 100 for v in tr[i, [6, 7, 0, 1, 2, 3, 4, 5]]])
+
+if prof.sum() > 0:
+    names = ["wait data", "row pass", "CSC pass", "flush", "release", "loop/other"]
+    print("consumer warp-cycles (all CTAs):", {nm: f"{v / prof.sum() * 100:.1f}%" for nm, v in zip(names, prof)})
