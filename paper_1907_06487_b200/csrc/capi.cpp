@@ -401,6 +401,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   A.slots = d_slots;
   A.runs = d_runs;
   A.spill_buf = d_spill;
+  A.check_n = n;
   A.block_cap = block_cap;
   A.window_cap = window_cap;
   A.nnz_cap = nnz_cap;

@@ -109,6 +109,7 @@ struct TiledArgs {
   double* spill_buf;              // K3: staged contributions to other tiles' rows
   int32_t block_cap, window_cap, nnz_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)
+  int32_t check_n;                // K4_CHECK builds: length of the x / y vectors
   unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
   int32_t debug_skip;             // diagnostics only (env SYMM_DEBUG_SKIP): skip bit0 row part,
                                   // bit1 CSC part, bit2 flush, bit3 spill-x gather (wrong results)

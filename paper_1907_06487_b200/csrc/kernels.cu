@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
       const int nfull = T > p ? ((T - p) & ~1) : 0;
       double* xs = reinterpret_cast<double*>(sm + s * slot_bytes + A.block_cap) + p;
+#ifdef K4_CHECK
+      if (T + p > A.window_cap || row0 + T > A.check_n) { printf("K4_CHECK own t=%d T=%d\n", t, T); __trap(); }
+#endif
       // own rows: the 16-B aligned part of x[row0 .. row0+T) by one bulk copy,
       // the (at most two) unaligned edge elements by cp.async
       if (lane == 2 && nfull > 0) {
@@ -388,6 +391,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
           for (int u = 0; u < 8; ++u) {
             const int len = R[u].z;  // (row, wid, len, 0)
             if (len <= 0) continue;
+#ifdef K4_CHECK
+            if (R[u].y + len + p > A.window_cap || R[u].x < 0 || R[u].x + len > A.check_n || R[u].y < T) {
+              printf("K4_CHECK run t=%d r=%d row=%d wid=%d len=%d T=%d wcap=%d n=%d\n", t, u, R[u].x, R[u].y, len, T, A.window_cap, A.check_n);
+              __trap();
+            }
+#endif
             double* dst = xs + R[u].y;
             const double* src = x + R[u].x;
             const int i0 = (int)(((uintptr_t)src >> 3) & 1);  // dst has the same 16-B phase
@@ -410,6 +419,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
 #pragma unroll 4
         for (int idx = lane; idx < S; idx += 32) {
           const int g = tgt[idx];
+#ifdef K4_CHECK
+          if (g >= A.check_n || T + idx + p >= A.window_cap) { printf("K4_CHECK loose t=%d g=%d idx=%d\n", t, g, idx); __trap(); }
+#endif
           if (g >= 0) cp_async8(xs + T + idx, x + g);
         }
       }
@@ -425,6 +437,16 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
+    // The loader takes stages in order; only once it has taken the stage for
+    // tile k are the previous uses of blk_full[s] / x_full[s] complete, so a
+    // parity wait cannot alias a phase two uses back (a group may finish its
+    // previous tile before an older tile's block has landed).
+    while (true) {
+      int lk;
+      asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(lk) : "r"(smem_u32(&loader_k)) : "memory");
+      if (lk > k) break;
+      __nanosleep(32);
+    }
     mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));  // TMA data visible to this thread
     mbar_wait(&x_full[s], (unsigned)((k / NS) & 1));
     if (gt == 0) TRACE(k, 3);
@@ -461,6 +483,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         // diagnostics: no flush
       } else if (ATOMIC) {
         const int gr = l < T ? row0 + l : tgt[l - T];
+#ifdef K4_CHECK
+        if (gr >= A.check_n) { printf("K4_CHECK flush t=%d l=%d gr=%d\n", t, l, gr); __trap(); }
+#endif
         if (gr >= 0) atomicAdd(y + gr, acc);  // -1: pad slot of the spill window
       } else if (l < T) {
         y[row0 + l] = acc;
