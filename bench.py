@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="st27_128")
-    ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "auto"])
+    ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "auto"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-variants", action="store_true", help="also time the other variants (extra key)")
@@ -133,6 +133,11 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def spmv_min_bytes(n: int, nnz_full: int) -> int:
+    """Eq. 2 at alpha = 1/NNZR: 12 B per full nonzero, row pointers, x once, y written."""
+    return 12 * nnz_full + 4 * (n + 1) + 16 * n
 
 
 def nnz_full_of(U):
@@ -383,16 +388,22 @@ def main():
     gflops_rank = 2.0 * nf / t_s / 1e9
     value = gflops_rank * ws  # replicas: every rank multiplies its own copy
     peak, peak_src = peaks()
+    if variant == "spmv":  # the yardstick streams the full matrix (Eq. 2)
+        bytes_min = spmv_min_bytes(n, nf)
     achieved = bytes_min / t_s / 1e9
     y_timed = ys[(a.steps - 1) % R].cpu().numpy()[perm]
 
     extra = {}
     if a.all_variants:
-        for v in ("atomic", "colored", "tiled", "tiled_atomic"):
+        for v in ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem", "spmv"):
             try:
                 m, l, _ = timed(v, max(50, a.steps // 4), 5)
                 extra[v] = {"ms_per_step": m, "gflops": 2.0 * nf / (m / 1e3) / 1e9,
                             "hbm_frac": bytes_min / (m / 1e3) / 1e9 / peak, "launches_per_step": l / max(50, a.steps // 4)}
+                if v == "spmv":  # the yardstick against its own Eq. 2 bytes (alpha = 1/NNZR)
+                    sb = spmv_min_bytes(n, nf)
+                    extra[v].update({"spmv_bytes_min": sb, "hbm_frac_spmv_model": sb / (m / 1e3) / 1e9 / peak,
+                                     "symmspmv_speedup": m / ms_step})
             except Exception as e:  # noqa: BLE001
                 extra[v] = {"error": str(e)}
 

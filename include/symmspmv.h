@@ -144,9 +144,12 @@ typedef enum {
   SYMM_VARIANT_ATOMIC = 2,  /* K1: one launch, native fp64 RED for transposed updates */
   SYMM_VARIANT_TILED = 3,   /* K3: TMA-staged tiles, smem two-pass, staged fixup; deterministic */
   SYMM_VARIANT_TILED_ATOMIC = 4,/* K4: same tiles, window flushed with fp64 RED into zeroed y */
-  SYMM_VARIANT_COLORED_SMEM = 5 /* K5: RACE write-set colours run inside a shared-memory x/y window
+  SYMM_VARIANT_COLORED_SMEM = 5,/* K5: RACE write-set colours run inside a shared-memory x/y window
                                    (plain smem read-modify-write, one barrier per colour); window
                                    flushed with fp64 RED into zeroed y                        */
+  SYMM_VARIANT_SPMV = 6         /* the paper's yardstick (Alg. 1): the same y := A x
+                                   from the FULL matrix A = U + U^T - diag(U) in CRS, the plan
+                                   mirrors U; deterministic, no atomics   */
 } symm_variant;
 
 typedef enum { SYMM_ORDER_PERMUTED = 0, SYMM_ORDER_ORIGINAL = 1 } symm_vec_order;

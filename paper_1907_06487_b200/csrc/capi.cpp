@@ -60,6 +60,12 @@ struct symmspmv_plan {
   int tiled_occ = 0;
   int32_t* d_in_ptr = nullptr;
   FixupArgs fargs{};
+  // K6 full-matrix SpMV (yardstick)
+  bool has_spmv = false;
+  int32_t *d_frp = nullptr, *d_fcol = nullptr;
+  double* d_fval = nullptr;
+  int spmv_vec = 8;
+  int64_t spmv_nnz = 0;
   // K5 colored_smem
   bool has_cs = false;
   CsArgs cargs{};
@@ -421,6 +427,53 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   return SYMM_OK;
 }
 
+// K6: the full matrix A' = U' + U'^T - diag(U') of the permuted order in CRS
+// (columns ascending per row), for the Alg. 1 yardstick.
+int build_spmv(symmspmv_plan_t* P, const Schedule& S) {
+  const int32_t n = S.n;
+  std::vector<int64_t> cnt((size_t)n + 1, 0);
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+      cnt[(size_t)r + 1]++;
+      if (S.pcol[(size_t)i] != r) cnt[(size_t)S.pcol[(size_t)i] + 1]++;
+    }
+  for (int32_t r = 0; r < n; ++r) cnt[(size_t)r + 1] += cnt[(size_t)r];
+  if (cnt[(size_t)n] >= ((int64_t)1 << 31)) return set_error(SYMM_ERR_OVERFLOW, "full matrix has >= 2^31 entries");
+  std::vector<int32_t> rp((size_t)n + 1), col((size_t)cnt[(size_t)n]);
+  std::vector<double> val((size_t)cnt[(size_t)n]);
+  for (int32_t r = 0; r <= n; ++r) rp[(size_t)r] = (int32_t)cnt[(size_t)r];
+  {
+    // lower part first (rows r get (r, c) for c < r from U' rows c), then the upper row
+    std::vector<int32_t> pos(rp.begin(), rp.end() - 1);
+    for (int32_t c = 0; c < n; ++c)
+      for (int32_t i = S.prow_ptr[(size_t)c]; i < S.prow_ptr[(size_t)c + 1]; ++i) {
+        const int32_t r = S.pcol[(size_t)i];
+        if (r == c) continue;
+        col[(size_t)pos[(size_t)r]] = c;  // ascending c by construction
+        val[(size_t)pos[(size_t)r]++] = S.pval[(size_t)i];
+      }
+    for (int32_t r = 0; r < n; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+        col[(size_t)pos[(size_t)r]] = S.pcol[(size_t)i];
+        val[(size_t)pos[(size_t)r]++] = S.pval[(size_t)i];
+      }
+  }
+  int rc;
+  if ((rc = upload(P, &P->d_frp, rp.data(), rp.size())) || (rc = upload(P, &P->d_fcol, col.data(), col.size())) ||
+      (rc = upload(P, &P->d_fval, val.data(), val.size())))
+    return rc;
+  P->spmv_nnz = (int64_t)col.size();
+  {  // lanes per row: the largest power of two <= NNZR / 1.5 (measured on B200: st27 16, kNN 8, 7-pt 4)
+    const double avg = n > 0 ? (double)P->spmv_nnz / n : 1.0;
+    int v = 1;
+    while (v < 32 && 2.0 * v <= avg / 1.5) v *= 2;
+    P->spmv_vec = v;
+  }
+  if (const char* v = std::getenv("SYMM_SPMV_VEC")) P->spmv_vec = std::atoi(v);
+  P->has_spmv = true;
+  return SYMM_OK;
+}
+
 // K5 format (cs_build.cpp); single rank.
 int build_cs(symmspmv_plan_t* P, const Schedule& S) {
   const int32_t nt = (int32_t)S.tile_group.size();
@@ -535,6 +588,11 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, true, st)))
       return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
     P->last_launches = 2;
+  } else if (variant == SYMM_VARIANT_SPMV) {
+    if (!P->has_spmv) return set_error(SYMM_ERR_ARG, "variant SPMV was not uploaded by this plan");
+    CsrArgs A{P->n, P->d_frp, P->d_fcol, P->d_fval};
+    if ((rc = launch_spmv(A, x, y, P->spmv_vec, P->sms, st))) return cuda_fail((cudaError_t)rc, "k_spmv");
+    P->last_launches = 1;
   } else if (variant == SYMM_VARIANT_COLORED_SMEM) {
     if (!P->has_cs) return set_error(SYMM_ERR_ARG, "variant COLORED_SMEM was not uploaded by this plan");
     if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
@@ -712,7 +770,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   if (U && (U->n != S.n || U->nnz != S.nnz))
     return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
                      (long long)U->nnz, S.n, (long long)S.nnz);
-  if (opt.variant < 0 || opt.variant > 5) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
+  if (opt.variant < 0 || opt.variant > 6) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
   if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks)
     return set_error(SYMM_ERR_ARG, "rank %d of %d", opt.rank, opt.nranks);
   if (opt.nranks > 1 && opt.variant != SYMM_VARIANT_TILED_ATOMIC && opt.variant != SYMM_VARIANT_AUTO)
@@ -752,8 +810,9 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   bool want_col = all || v == SYMM_VARIANT_COLORED;
   bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
   bool want_cs = all || v == SYMM_VARIANT_COLORED_SMEM;
+  bool want_spmv = all || v == SYMM_VARIANT_SPMV;
   if (opt.nranks > 1) {
-    want_col = want_csr = want_cs = false;
+    want_col = want_csr = want_cs = want_spmv = false;
     P->variant = SYMM_VARIANT_TILED_ATOMIC;
   }
   if (want_tiled) {
@@ -777,6 +836,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   }
   if (!rc && want_col) rc = build_colored(P, S);
   if (!rc && want_cs) rc = build_cs(P, S);
+  if (!rc && want_spmv) rc = build_spmv(P, S);
   if (!rc) {
     if (!(rc = upload(P, &P->d_perm, S.perm.data(), S.perm.size())) &&
         !(rc = upload(P, &P->d_inv, S.inv.data(), S.inv.size())) && !(rc = dev_alloc(P, &P->d_xp, (size_t)S.n)))

@@ -201,6 +201,9 @@ int cs_smem_bytes(const CsArgs& A);
 int cs_configure(CsArgs& A, int* ctas_per_sm, int nc);   // sets the smem attribute, returns occupancy
 int launch_cs(const CsArgs& A, const double* x, double* y, int grid, int nc, void* stream);
 
+// full-matrix SpMV (Alg. 1) on the mirrored permuted CRS
+int launch_spmv(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream);
+
 // kernel launchers (kernels.cu); return cudaError_t as int
 int launch_zero(double* y, int64_t n, void* stream);
 int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream);

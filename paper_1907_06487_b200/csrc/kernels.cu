@@ -114,6 +114,30 @@ __global__ void __launch_bounds__(256) k_atomic(CsrArgs A, const double* __restr
   }
 }
 
+// ---------------------------------------------------------------- K6 SpMV (yardstick)
+// Alg. 1 on the full CRS: V lanes per row stream the row's
+// (col, val) pairs with non-allocating loads, gather x through L1/L2, reduce
+// by shuffles and store y[row] once (no atomics, deterministic).
+template <int V>
+__global__ void __launch_bounds__(256) k_spmv(CsrArgs A, const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int RPW = 32 / V;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % V;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * RPW; base < A.n; base += nwarps * RPW) {  // warp-uniform
+    const int64_t row = base + lane / V;
+    double sum = 0.0;
+    if (row < A.n) {
+      const int b = A.row_ptr[row], e = A.row_ptr[row + 1];
+#pragma unroll 4
+      for (int i = b + sub; i < e; i += V) sum += ld_stream_f64(A.val + i) * __ldg(x + ld_stream_i32(A.col + i));
+    }
+    sum = group_sum<V>(sum);
+    if (row < A.n && sub == 0) y[row] = sum;
+  }
+}
+
 // ---------------------------------------------------------------- K2 colored
 template <int V>
 __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const double* __restrict__ x,
@@ -861,6 +885,25 @@ int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms
     case 8: k_atomic<8><<<grid, threads, 0, st>>>(A, x, y); break;
     case 16: k_atomic<16><<<grid, threads, 0, st>>>(A, x, y); break;
     default: k_atomic<32><<<grid, threads, 0, st>>>(A, x, y); break;
+  }
+  return (int)cudaGetLastError();
+}
+
+int launch_spmv(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream) {
+  if (A.n <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = 256;
+  int64_t warps_needed = ((int64_t)A.n * vec + 31) / 32;
+  int64_t g = (warps_needed * 32 + threads - 1) / threads;
+  int64_t gmax = (int64_t)sms * 8;
+  int grid = (int)(g < gmax ? (g < 1 ? 1 : g) : gmax);
+  switch (vec) {
+    case 1: k_spmv<1><<<grid, threads, 0, st>>>(A, x, y); break;
+    case 2: k_spmv<2><<<grid, threads, 0, st>>>(A, x, y); break;
+    case 4: k_spmv<4><<<grid, threads, 0, st>>>(A, x, y); break;
+    case 8: k_spmv<8><<<grid, threads, 0, st>>>(A, x, y); break;
+    case 16: k_spmv<16><<<grid, threads, 0, st>>>(A, x, y); break;
+    default: k_spmv<32><<<grid, threads, 0, st>>>(A, x, y); break;
   }
   return (int)cudaGetLastError();
 }
