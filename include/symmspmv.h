@@ -83,6 +83,15 @@ typedef struct {
   int32_t min_group_levels; /* >= k: minimum levels per level group ("at least k") */
   int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
   uint32_t flags;           /* bit 0: within-level order = original index (experimental)    */
+  int32_t scheme;           /* 0 = RACE (levels, groups, tiles: the default);
+                               1 = MC: greedy distance-2 (write-set) colouring of single rows,
+                                   rows ordered colour by colour;
+                               2 = ABMC: blocks of `abmc_block` consecutive BFS-ordered rows,
+                                   blocks coloured by their write sets and ordered colour by colour
+                                   (contiguous blocks stand in for METIS parts).
+                               MC / ABMC colour classes become the level groups and phases; they
+                               exist to reproduce the paper's comparison. */
+  int32_t abmc_block;       /* rows per ABMC block (default 64)                               */
 } race_config;
 
 typedef struct race_schedule race_schedule_t;

@@ -27,7 +27,7 @@ class RaceConfig(C.Structure):
                 ("root", C.c_int32), ("n_eps", C.c_int32), ("eps", C.c_double * 8), ("max_tile_rows", C.c_int32),
                 ("max_tile_window", C.c_int32), ("max_tile_nnz", C.c_int32), ("reorder", C.c_int32), ("cone_tiles", C.c_int32),
                 ("min_group_levels", C.c_int32), ("validate", C.c_int32),
-                ("flags", C.c_uint32)]
+                ("flags", C.c_uint32), ("scheme", C.c_int32), ("abmc_block", C.c_int32)]
 
 
 class RaceScheduleStats(C.Structure):

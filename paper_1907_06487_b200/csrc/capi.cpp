@@ -648,6 +648,8 @@ void race_config_default(race_config* c) {
   c->min_group_levels = 2;
   c->validate = 1;
   c->flags = 0;
+  c->scheme = 0;
+  c->abmc_block = 64;
 }
 
 int race_build_schedule(const symm_csr_upper* U, const race_config* cfg, race_schedule_t** out) {

@@ -351,7 +351,8 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   else race_config_default(&cfg);
   if (cfg.k < 2) return set_error(SYMM_ERR_K, "distance k = %d < 2: SymmSpMV needs distance-2 (PAPER.md:787-789)", cfg.k);
   if (cfg.tile_work <= 0 || cfg.max_tile_rows <= 0 || cfg.max_tile_rows > 65535 || cfg.max_tile_window < 64 ||
-      cfg.max_tile_window > 65535 || cfg.max_tile_nnz < 1 || cfg.max_tile_nnz > 65535 || cfg.n_eps < 1 || cfg.n_eps > 8 || cfg.n_workers < 0)
+      cfg.max_tile_window > 65535 || cfg.max_tile_nnz < 1 || cfg.max_tile_nnz > 65535 || cfg.n_eps < 1 || cfg.n_eps > 8 || cfg.n_workers < 0 ||
+      cfg.scheme < 0 || cfg.scheme > 2 || (cfg.scheme == 2 && cfg.abmc_block < 1))
     return set_error(SYMM_ERR_ARG, "invalid race_config field");
   int rc = validate_upper(U);
   if (rc) return rc;
@@ -478,6 +479,59 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     S->bw_after = bwa;
   };
   build_permuted();
+  if (cfg.scheme != 0) {
+    // ---- NEXT-3 comparison schemes: MC colours single rows,
+    // ABMC colours blocks of consecutive BFS-ordered rows; both greedy in BFS
+    // order by closed neighbourhoods N[v] = {v} ∪ adj(v) -- the distance-2
+    // relation of PAPER.md:787-789 in its order-independent form (any
+    // orientation's write set {r} ∪ {upper columns} lies inside N[r], so the
+    // colouring stays valid after the rows are re-ordered colour by colour).
+    // Each colour class then becomes one level and one level group, so the
+    // tiles, phases and validators below apply unchanged.
+    const int32_t B = cfg.scheme == 1 ? 1 : cfg.abmc_block;
+    const int32_t nb = (n + B - 1) / B;
+    std::vector<int32_t> bcol((size_t)nb, 0), last((size_t)n, -1);  // last[v] = newest colour writing v
+    std::vector<std::vector<int32_t>> writers((size_t)n);            // colours writing v so far (original ids)
+    int32_t ncol = 0;
+    {
+      std::vector<uint64_t> used;
+      for (int32_t b = 0; b < nb; ++b) {
+        used.assign((size_t)(ncol / 64 + 2), 0);
+        const int32_t r0b = b * B, r1b = std::min(n, r0b + B);
+        for (int32_t r = r0b; r < r1b; ++r) {
+          const int32_t v = S->inv[(size_t)r];
+          for (int64_t e = gp[(size_t)v] - 1; e < gp[(size_t)v + 1]; ++e) {
+            const int32_t c = e < gp[(size_t)v] ? v : ga[(size_t)e];
+            for (int32_t q : writers[(size_t)c]) used[(size_t)q / 64] |= uint64_t(1) << (q % 64);
+          }
+        }
+        int32_t col = 0;
+        while (used[(size_t)col / 64] >> (col % 64) & 1) ++col;
+        bcol[(size_t)b] = col;
+        ncol = std::max(ncol, col + 1);
+        for (int32_t r = r0b; r < r1b; ++r) {
+          const int32_t v = S->inv[(size_t)r];
+          for (int64_t e = gp[(size_t)v] - 1; e < gp[(size_t)v + 1]; ++e) {
+            const int32_t c = e < gp[(size_t)v] ? v : ga[(size_t)e];
+            if (last[(size_t)c] != col) {
+              writers[(size_t)c].push_back(col);
+              last[(size_t)c] = col;
+            }
+          }
+        }
+      }
+    }
+    std::vector<int32_t> cstart((size_t)ncol + 1, 0);
+    for (int32_t b = 0; b < nb; ++b) cstart[(size_t)bcol[(size_t)b] + 1] += std::min(n, b * B + B) - b * B;
+    for (int32_t c = 0; c < ncol; ++c) cstart[(size_t)c + 1] += cstart[(size_t)c];
+    std::vector<int32_t> pos(cstart.begin(), cstart.end() - 1), inv2((size_t)n);
+    for (int32_t b = 0; b < nb; ++b)
+      for (int32_t r = b * B; r < std::min(n, b * B + B); ++r) inv2[(size_t)pos[(size_t)bcol[(size_t)b]]++] = S->inv[(size_t)r];
+    S->inv.swap(inv2);
+    for (int32_t f = 0; f < n; ++f) S->perm[(size_t)S->inv[(size_t)f]] = f;
+    build_permuted();
+    S->level_ptr = cstart;  // one "level" per colour class
+  }
   const int32_t* rp = S->prow_ptr.data();  // re-bound after the cone re-permutation
   const int32_t* pc = S->pcol.data();
 
@@ -495,6 +549,14 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     total_work += w;
   }
   int64_t nworkers = cfg.n_workers > 0 ? cfg.n_workers : std::max<int64_t>(1, (total_work + cfg.tile_work - 1) / cfg.tile_work);
+  if (cfg.scheme != 0) {
+    // MC / ABMC: every colour class is its own group, split into tiles by work
+    S->group_lvl.resize((size_t)totalLvl + 1);
+    for (int32_t l = 0; l <= totalLvl; ++l) S->group_lvl[(size_t)l] = l;
+    S->group_workers.resize((size_t)totalLvl);
+    for (int32_t l = 0; l < totalLvl; ++l)
+      S->group_workers[(size_t)l] = (int32_t)std::max<int64_t>(1, (lw[(size_t)l] + cfg.tile_work - 1) / cfg.tile_work);
+  } else {
   S->windows = eps_aggregate(lw, nworkers, kg, cfg.eps[0]);
   {
     std::vector<int32_t> T, wk;
@@ -511,6 +573,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     if (T.size() >= 3) alg4_balance(T, wk, lw, kg);
     S->group_lvl = T;
     S->group_workers = wk;
+  }
   }
   const int32_t ngroups = (int32_t)S->group_workers.size();
 

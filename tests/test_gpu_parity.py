@@ -205,3 +205,13 @@ def test_multirank_plans_emulated_on_one_gpu(name, ws):
         for (q, a, c) in halo_pieces(b, h, p):
             y[a:c] += yl[p][a - b[p]:c - b[p]]
     assert relinf(y[perm], y_ref) <= TOL
+
+
+@pytest.mark.parametrize("scheme,block", [(1, 1), (2, 16), (2, 64)])
+@pytest.mark.parametrize("variant", ["colored", "tiled_atomic", "tiled"])
+def test_mc_abmc_schedules(scheme, block, variant):
+    """NEXT-3: the MC / ABMC comparison schedules run through the same kernels."""
+    U, x = gen.make_config("st27_24")
+    y_ref = oracle.symmspmv(U, x)
+    outs, _, _ = run_gpu(U, x, variant, sched_kw=dict(scheme=scheme, abmc_block=block))
+    assert relinf(outs[0], y_ref) <= TOL
