@@ -9,6 +9,7 @@ CC ?= gcc
 # host C++ compiler with OpenMP: the first of $(CXX), g++, /usr/bin/g++ that
 # links -fopenmp (some images point CXX at a wrapper without libgomp.spec)
 OMPCXX := $(shell for c in $(CXX) g++ /usr/bin/g++; do echo 'int main(){return 0;}' | $$c -fopenmp -x c++ - -o /dev/null >/dev/null 2>&1 && { echo $$c; break; }; done)
+OMPCC := $(shell for c in $(CC) gcc /usr/bin/gcc; do echo 'int main(){return 0;}' | $$c -fopenmp -x c - -o /dev/null >/dev/null 2>&1 && { echo $$c; break; }; done)
 ifeq ($(OMPCXX),)
 $(error no host C++ compiler with OpenMP support found)
 endif
@@ -27,7 +28,7 @@ gen/libsymmgen.so: gen/symmgen.cpp
 
 # -ffp-contract=off: no FMA contraction in the oracle (reading R5)
 oracle/liboracle.so: oracle/oracle.c
-	$(CC) -O2 -std=c99 -ffp-contract=off -fPIC -shared -Wall -o $@ $<
+	$(OMPCC) -O2 -std=c99 -ffp-contract=off -fopenmp -fPIC -shared -Wall -o $@ $<
 
 $(CSRC)/schedule.o: $(CSRC)/schedule.cpp $(PROD_HDRS)
 	$(OMPCXX) -O3 -std=c++17 -fopenmp -fPIC -Wall -Iinclude -c -o $@ $<

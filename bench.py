@@ -163,6 +163,25 @@ def cpu_baseline(U, x, seconds: float, nnz_full: int, label: str):
             "seconds_per_step": per, "y": y}
 
 
+def cpu_baseline_omp(U, x, seconds: float, nnz_full: int, label: str):
+    """The OpenMP oracle (Alg. 2 with thread-private target arrays) on all host cores."""
+    import oracle
+
+    oracle.symmspmv_omp(U, x)  # first touch of the private arrays
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        _, nt = oracle.symmspmv_omp(U, x)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    per = el / reps
+    return {"value": 2.0 * nnz_full / per / 1e9, "unit": "GFLOP/s", "cores": nt, "kind": "oracle_openmp",
+            "sample": f"{reps} full OpenMP oracle SymmSpMV multiplies of {label} ({el:.1f} s, {nt} threads)",
+            "seconds_per_step": per}
+
+
 def run_reference(a):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -193,7 +212,9 @@ def run_reference(a):
             "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": a.config, "n": U.n, "nnz_upper": int(U.nnz), "nnz_full": nf},
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{len(times)} serial oracle multiplies of {a.config} (capped at {budget:.0f} s)"},
+                             "sample": f"{len(times)} serial oracle multiplies of {a.config} (capped at {budget:.0f} s)",
+                             "openmp": {k: v for k, v in cpu_baseline_omp(U, x, 5.0, nf, a.config).items()
+                                        if k != "seconds_per_step"}},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -428,6 +449,8 @@ def main():
         # with the last timed GPU output on sampled rows
         cb = cpu_baseline(U, x, a.cpu_seconds, nf, a.config)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu["openmp"] = {k: v for k, v in cpu_baseline_omp(U, x, max(2.0, a.cpu_seconds / 2), nf, a.config).items()
+                         if k != "seconds_per_step"}
         y_ref = cb["y"]
         sample = np.random.default_rng(0).choice(n, size=min(n, 4096), replace=False)
         err = float(np.max(np.abs(y_timed[sample] - y_ref[sample])) / np.max(np.abs(y_ref)))

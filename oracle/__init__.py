@@ -38,6 +38,8 @@ def _lib():
         L.oracle_symmspmv.restype = None
         L.oracle_symmspmv_ld.argtypes = [i32, vp, vp, vp, vp, vp]
         L.oracle_symmspmv_ld.restype = None
+        L.oracle_symmspmv_omp.argtypes = [i32, vp, vp, vp, vp, vp, i32]
+        L.oracle_symmspmv_omp.restype = i32
         L.oracle_mirror.argtypes = [i32, vp, vp, vp, vp, vp, vp]
         L.oracle_mirror.restype = i64
         L.oracle_spmv.argtypes = [i32, vp, vp, vp, vp, vp]
@@ -70,6 +72,18 @@ def symmspmv(U, x) -> np.ndarray:
     y = np.empty(U.n, dtype=np.float64)
     _lib().oracle_symmspmv(U.n, _p(rp), _p(col), _p(val), _p(x), _p(y))
     return y
+
+
+def symmspmv_omp(U, x, nthreads: int = 0):
+    """Alg. 2 with thread-private target arrays (PAPER.md:189-191), OpenMP;
+    returns (y, threads used).  Host-core baseline for bench.py only."""
+    rp, col, val = _csr(U)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(U.n, dtype=np.float64)
+    nt = _lib().oracle_symmspmv_omp(U.n, _p(rp), _p(col), _p(val), _p(x), _p(y), int(nthreads))
+    if nt < 0:
+        raise MemoryError("oracle_symmspmv_omp: allocation failed")
+    return y, nt
 
 
 def symmspmv_ld(U, x) -> np.ndarray:

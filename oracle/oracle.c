@@ -7,7 +7,8 @@
  * cpu_baseline / --impl reference legs may load this library.  It shares no
  * code, header, table or helper with the product (paper_1907_06487_b200/).
  *
- * Every routine is single-threaded, fp64 (or long double where stated), with
+ * Every routine except oracle_symmspmv_omp (the OpenMP host baseline) is
+ * single-threaded, fp64 (or long double where stated), with
  * no blocking, fusion or reordering beyond the algorithm it cites.
  * Citations are PAPER.md line ranges with the section / algorithm label.
  *
@@ -18,6 +19,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <omp.h>
 
 /* ---------------------------------------------------------------------------
  * Alg. 2 "SymmSpMV b = A x, where A is an upper triangular matrix"
@@ -43,6 +45,74 @@ void oracle_symmspmv(int32_t n, const int32_t* rowPtr, const int32_t* col, const
     }
     b[row] += tmp;                          /* b[row] += tmp                   */
   }
+}
+
+/* ---------------------------------------------------------------------------
+ * OpenMP version of Alg. 2 (the host-core baseline the north star asks for),
+ * parallelised the way PAPER.md:189-191 names as the general solution:
+ * "thread private target arrays".  Rows are split into `nthreads` contiguous
+ * blocks of equal row count (OpenMP static schedule); thread t runs Alg. 2
+ * unchanged on its block into a private array b_t covering the rows its block
+ * can write, [first row of the block, 1 + largest column in the block); then
+ * b[i] = sum over t (ascending) of b_t[i].  nthreads <= 0 uses the OpenMP
+ * default.  Returns the number of threads used (-1 on allocation failure).
+ * With one thread it is oracle_symmspmv bit for bit.
+ * ------------------------------------------------------------------------- */
+int32_t oracle_symmspmv_omp(int32_t n, const int32_t* rowPtr, const int32_t* col, const double* A,
+                            const double* x, double* b, int32_t nthreads) {
+  int32_t nt = nthreads > 0 ? nthreads : omp_get_max_threads();
+  if (nt > n) nt = n > 0 ? n : 1;
+  int32_t* lo = (int32_t*)malloc(sizeof(int32_t) * (size_t)nt);
+  int32_t* hi = (int32_t*)malloc(sizeof(int32_t) * (size_t)nt);
+  double** bt = (double**)calloc((size_t)nt, sizeof(double*));
+  int failed = (lo == NULL || hi == NULL || bt == NULL);
+  if (!failed) {
+#pragma omp parallel num_threads(nt)
+    {
+      int32_t t = omp_get_thread_num();
+      int32_t r0 = (int32_t)((int64_t)n * t / nt), r1 = (int32_t)((int64_t)n * (t + 1) / nt);
+      int32_t h = r0;
+      for (int32_t row = r0; row < r1; ++row)
+        for (int32_t idx = rowPtr[row]; idx < rowPtr[row + 1]; ++idx)
+          if (col[idx] + 1 > h) h = col[idx] + 1;
+      if (r1 > h) h = r1;
+      lo[t] = r0;
+      hi[t] = h;
+      double* bl = (double*)malloc(sizeof(double) * (size_t)(h - r0 > 0 ? h - r0 : 1));
+      bt[t] = bl;
+      if (bl != NULL) {
+        for (int32_t i = r0; i < h; ++i) bl[i - r0] = 0.0;
+        for (int32_t row = r0; row < r1; ++row) {   /* Alg. 2 on the block, into b_t */
+          int32_t start = rowPtr[row];
+          if (start < rowPtr[row + 1] && col[start] == row) {
+            bl[row - r0] += A[start] * x[row];
+            start += 1;
+          }
+          double tmp = 0.0;
+          for (int32_t idx = start; idx < rowPtr[row + 1]; ++idx) {
+            tmp += A[idx] * x[col[idx]];
+            bl[col[idx] - r0] += A[idx] * x[row];
+          }
+          bl[row - r0] += tmp;
+        }
+      }
+#pragma omp barrier
+#pragma omp for schedule(static)
+      for (int32_t i = 0; i < n; ++i) {              /* b[i] = sum_t b_t[i], t ascending */
+        double s = 0.0;
+        for (int32_t u = 0; u < nt; ++u)
+          if (bt[u] != NULL && i >= lo[u] && i < hi[u]) s += bt[u][i - lo[u]];
+        b[i] = s;
+      }
+    }
+    for (int32_t u = 0; u < nt; ++u) failed |= (bt[u] == NULL);
+  }
+  if (bt != NULL)
+    for (int32_t u = 0; u < nt; ++u) free(bt[u]);
+  free(bt);
+  free(lo);
+  free(hi);
+  return failed ? -1 : nt;
 }
 
 /* Same algorithm with long double accumulation everywhere ("reference grade",

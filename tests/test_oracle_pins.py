@@ -105,6 +105,31 @@ def test_spec_hand_cases():
     assert np.array_equal(oracle.symmspmv(U, np.array([1.0, 1.0, 1.0])), [1.0, 10.0, 2.0])
 
 
+@pytest.mark.parametrize("mk", SMALL)
+@pytest.mark.parametrize("nt", [1, 2, 3, 8])
+def test_symmspmv_omp_thread_private(mk, nt):
+    """OpenMP host baseline (thread-private target arrays):
+    one thread is Alg. 2 bit for bit; any thread count is y = A x (dense brute force)."""
+    U = mk()
+    x = gen.vector_uniform(U.n, 11)
+    y, used = oracle.symmspmv_omp(U, x, nt)
+    assert used == min(nt, U.n)
+    if nt == 1:
+        assert np.array_equal(y, oracle.symmspmv(U, x))
+    assert relinf(y, oracle.to_dense(U) @ x) <= 1e-14
+
+
+def test_symmspmv_omp_edge_cases():
+    U = gen.from_edges(1, [], [], [], [2.5])
+    y, used = oracle.symmspmv_omp(U, np.array([4.0]), 4)
+    assert used == 1 and y[0] == 10.0
+    # a star: row 0 writes every row, so block 0's private array spans all of them
+    U = gen.from_edges(50, [0] * 49, list(range(1, 50)))
+    x = gen.vector_uniform(50, 2)
+    y, _ = oracle.symmspmv_omp(U, x, 7)
+    assert relinf(y, oracle.to_dense(U) @ x) <= 1e-14
+
+
 def test_empty_and_single():
     U = gen.from_edges(0, [], [], [], np.zeros(0))
     assert oracle.symmspmv(U, np.zeros(0)).shape == (0,)
