@@ -157,9 +157,32 @@ void partition_tiles(const Schedule& S, int nranks, std::vector<int32_t>& tile_b
   }
 }
 
+// Window id of column c in a tile [r0, r1) with spill runs tr[0..nrt):
+// own rows 0..T-1, spill targets through the runs; -1 if c is not in the window.
+static int32_t run_local(const SpillRun* tr, int32_t nrt, int32_t r0, int32_t r1, int32_t c) {
+  if (c >= r0 && c < r1) return c - r0;
+  int32_t lo = 0, hi = nrt;  // last run with first row <= c
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) / 2;
+    if (tr[mid].row <= c) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo == 0 || c >= tr[lo - 1].row + tr[lo - 1].len) return -1;
+  return tr[lo - 1].wid + (c - tr[lo - 1].row);
+}
+
 // K3/K4 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order;
 // a multi-rank plan keeps only its own tile range [t_begin, t_end).
-int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t t_end) {
+struct TiledHost {
+  std::vector<TileDesc> desc;
+  std::vector<unsigned char> blocks;
+  std::vector<int32_t> slot_tgt, slots, in_ptr;
+  std::vector<SpillRun> runs;
+  int64_t nsp = 0;
+  int32_t block_cap = 0, window_cap = 0, nnz_cap = 0;
+};
+
+int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHost& H) {
   const int32_t nt = (int32_t)S.tile_group.size();
   const int32_t n = S.n;
   std::vector<int32_t> tile_of((size_t)n);
@@ -222,6 +245,37 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
       prev = g;
     }
   }
+  // Per tile: lane positions in slot order, or sorted by descending work
+  // (row entries + transposed entries of the slot).  The kernel walks each
+  // lane's list (row part, then transposed part) in lock step with its warp
+  // (32 consecutive positions), so a warp costs its longest list; sorting is
+  // used when it saves at least `gain` of those lock steps (own-row REDs lose
+  // their coalescing, so a small saving is not worth it).
+  double gain = 0.25;
+  if (const char* v = std::getenv("SYMM_SORT_GAIN")) gain = std::atof(v);
+  std::vector<char> sort_tile((size_t)nt, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int32_t t = 0; t < nt; ++t) {
+    const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
+    const int32_t W = T + (int32_t)(slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
+    std::vector<int32_t> work((size_t)W, 0);
+    for (int32_t r = r0; r < r1; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+        const int32_t c = S.pcol[(size_t)i];
+        work[(size_t)(r - r0)] += 1;
+        if (c == r) continue;
+        const int32_t lc = run_local(runs.data() + run_ptr[(size_t)t], (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]), r0, r1, c);
+        if (lc >= 0 && lc < W) work[(size_t)lc] += 1;
+      }
+    auto steps = [&](const std::vector<int32_t>& w) {
+      int64_t s = 0;
+      for (int32_t g = 0; g < W; g += 32) s += *std::max_element(w.begin() + g, w.begin() + std::min(W, g + 32));
+      return s;
+    };
+    std::vector<int32_t> ws(work);
+    std::sort(ws.begin(), ws.end(), std::greater<int32_t>());
+    sort_tile[(size_t)t] = W > 32 && (double)steps(ws) <= (1.0 - gain) * (double)steps(work);
+  }
   int32_t block_cap = 16, window_cap = 2, nnz_cap = 2;
   int bad = 0;
   for (int32_t t = 0; t < nt; ++t) {
@@ -236,8 +290,11 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     int64_t o_lcol = align16(o_start + 2 * (int64_t)(T + 1));
     int64_t o_tidx = align16(o_lcol + 2 * nnz);
     int64_t o_tptr = align16(o_tidx + 4 * (nnz - nd));
-    int64_t o_tgt = align16(o_tptr + 2 * (W + 1));
-    int64_t o_slot = o_tgt;
+    // lane positions sorted by work when that shortens the warps' lock-step
+    // lists enough (decided below, per tile)
+    const int srt = sort_tile[(size_t)t];
+    int64_t o_sid = align16(o_tptr + 2 * (W + 1));
+    int64_t o_tgt = srt ? align16(o_sid + 2 * W) : o_sid;
     int64_t o_val = align16(o_tgt + 4 * (int64_t)S_);
     int64_t bytes = align16(o_val + 8 * nnz);
     if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
@@ -252,7 +309,8 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     D.o_tidx = (uint16_t)o_tidx;
     D.o_tptr = (uint16_t)o_tptr;
     D.o_tgt = (uint16_t)o_tgt;
-    D.o_slot = (uint16_t)o_slot;
+    D.o_sid = (uint16_t)o_sid;
+    D.sorted = srt;
     D.o_val = (uint16_t)o_val;
     D.spill_off = (int32_t)slot_ptr[(size_t)t];
     D.run_off = (int32_t)run_ptr[(size_t)t];
@@ -286,7 +344,6 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   for (int32_t t = 0; t < nt; ++t) {
     const TileDesc& D = desc[(size_t)t];
     const int32_t r0 = D.row0, T = D.nrows, r1 = r0 + T, ns = D.nspill, W = T + ns;
-    const int32_t* st = slot_tgt.data() + slot_ptr[(size_t)t];
     unsigned char* blk = blocks.data() + D.block_off;
     std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
     uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
@@ -295,40 +352,55 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
+    const int32_t* st = slot_tgt.data() + slot_ptr[(size_t)t];
     for (int32_t j = 0; j < ns; ++j) tgt[j] = st[j];  // flush target of every spill slot (-1 = pad)
     const int32_t e0 = S.prow_ptr[(size_t)r0];
-    // window id of a target: own rows 0..T-1; spill targets through the runs
     const SpillRun* tr = runs.data() + run_ptr[(size_t)t];
     const int32_t nrt = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
-    auto local = [&](int32_t c) -> int32_t {
-      if (c < r1) return c - r0;
-      int32_t lo = 0, hi = nrt;  // last run with first row <= c
-      while (lo < hi) {
-        int32_t mid = (lo + hi) / 2;
-        if (tr[mid].row <= c) lo = mid + 1;
-        else hi = mid;
+    const bool bank_aware = !std::getenv("SYMM_NO_BANK_ORDER");
+    // window id of every entry's column; list lengths of every slot
+    const int32_t nnz = D.nnz;
+    std::vector<int32_t> eloc((size_t)nnz);
+    std::vector<int32_t> rl((size_t)W, 0), cl((size_t)W, 0);
+    for (int32_t r = r0; r < r1; ++r) {
+      rl[(size_t)(r - r0)] = S.prow_ptr[(size_t)r + 1] - S.prow_ptr[(size_t)r];
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+        const int32_t lc = run_local(tr, nrt, r0, r1, S.pcol[(size_t)i]);
+        if (lc < 0) { bad |= 1; continue; }
+        eloc[(size_t)(i - e0)] = lc;
+        if (S.pcol[(size_t)i] != r) cl[(size_t)lc]++;
       }
-      if (lo == 0 || c >= tr[lo - 1].row + tr[lo - 1].len) {
-        bad |= 1;
-        return 0;
-      }
-      return tr[lo - 1].wid + (c - tr[lo - 1].row);
-    };
-    // row pass: the 32 consecutive rows of a warp are walked in lock step;
-    // order every row's entries so that at each step the x gathers of a half
-    // warp hit distinct bank pairs (window id mod 16)
+    }
+    // lane position -> window slot
+    std::vector<int32_t> slot_at((size_t)W);
+    for (int32_t i = 0; i < W; ++i) slot_at[(size_t)i] = i;
+    if (D.sorted) {
+      std::stable_sort(slot_at.begin(), slot_at.end(), [&](int32_t a, int32_t b) {
+        return rl[(size_t)a] + cl[(size_t)a] > rl[(size_t)b] + cl[(size_t)b];
+      });
+      uint16_t* sid = reinterpret_cast<uint16_t*>(blk + D.o_sid);
+      for (int32_t i = 0; i < W; ++i) sid[i] = (uint16_t)slot_at[(size_t)i];
+    }
+    // row part: a warp walks the lists of 32 consecutive lane positions in
+    // lock step; order every row's entries so that at each step the x
+    // gathers of a half warp hit distinct bank pairs (window id mod 16)
     std::vector<std::vector<std::pair<uint16_t, double>>> ent;
-    for (int32_t w0 = 0; w0 < T; w0 += 32) {
-      const int32_t w1 = std::min(T, w0 + 32);
-      ent.assign((size_t)(w1 - w0), {});
-      for (int32_t r = r0 + w0; r < r0 + w1; ++r)
-        for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i)
-          ent[(size_t)(r - r0 - w0)].push_back({(uint16_t)local(S.pcol[(size_t)i]), S.pval[(size_t)i]});
-      if (!std::getenv("SYMM_NO_BANK_ORDER")) bank_order_rows(ent, 1);
-      for (int32_t r = r0 + w0; r < r0 + w1; ++r) {
-        const auto& e = ent[(size_t)(r - r0 - w0)];
-        const int32_t b = S.prow_ptr[(size_t)r] - e0;
-        start[r - r0] = (uint16_t)b;
+    for (int32_t g0 = 0; g0 < W; g0 += 32) {
+      const int32_t g1 = std::min(W, g0 + 32);
+      ent.assign((size_t)(g1 - g0), {});
+      for (int32_t i = g0; i < g1; ++i) {
+        const int32_t l = slot_at[(size_t)i];
+        if (l >= T) continue;
+        for (int32_t k = S.prow_ptr[(size_t)(r0 + l)]; k < S.prow_ptr[(size_t)(r0 + l) + 1]; ++k)
+          ent[(size_t)(i - g0)].push_back({(uint16_t)eloc[(size_t)(k - e0)], S.pval[(size_t)k]});
+      }
+      if (bank_aware) bank_order_rows(ent, 1);
+      for (int32_t i = g0; i < g1; ++i) {
+        const int32_t l = slot_at[(size_t)i];
+        if (l >= T) continue;
+        const auto& e = ent[(size_t)(i - g0)];
+        const int32_t b = S.prow_ptr[(size_t)(r0 + l)] - e0;
+        start[l] = (uint16_t)b;
         for (size_t k = 0; k < e.size(); ++k) {
           lcol[b + (int32_t)k] = e[k].first;
           val[b + (int32_t)k] = e[k].second;
@@ -336,42 +408,61 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
       }
     }
     start[T] = (uint16_t)(S.prow_ptr[(size_t)r1] - e0);
-    // CSC pass: target l's list of (entry, local row); at each step the lanes
-    // of a half warp (32 consecutive targets) should read val[entry] and
-    // xs[row] from distinct bank pairs
+    // transposed part: slot l's list of (entry, local row), walked after the
+    // row part in the same lock step; at each step the lanes of a half warp
+    // should read val[entry] and xs[row] from bank pairs not used by the
+    // other lanes (including those still in their row part)
     std::vector<std::vector<uint32_t>> lists((size_t)W);
-    for (int32_t r = r0; r < r1; ++r)
-      for (int32_t k = start[r - r0]; k < start[r - r0 + 1]; ++k)
-        if (lcol[k] != r - r0) lists[lcol[k]].push_back((uint32_t)k | ((uint32_t)(r - r0) << 16));
+    for (int32_t l = 0; l < T; ++l)
+      for (int32_t k = start[l]; k < start[l + 1]; ++k)
+        if (lcol[k] != l) lists[lcol[k]].push_back((uint32_t)k | ((uint32_t)l << 16));
     const int32_t vb = (int32_t)(D.o_val / 8);  // bank-pair phase of val[0]
-    if (!std::getenv("SYMM_NO_BANK_ORDER"))
-      for (int32_t w0 = 0; w0 < W; w0 += 32) {
-        const int32_t w1 = std::min(W, w0 + 32);
-        size_t maxlen = 0;
-        for (int32_t l = w0; l < w1; ++l) maxlen = std::max(maxlen, lists[(size_t)l].size());
-        for (size_t j = 0; j < maxlen; ++j)
-          for (int32_t h = w0; h < w1; h += 16) {
+    // sorted tiles walk one list per lane (row part, then transposed part) in
+    // lock step; unsorted tiles walk the two parts as separate lock-step loops
+    const bool uni = D.sorted != 0;
+    auto rlen = [&](int32_t l) { return (uni && l < T) ? (int32_t)(start[l + 1] - start[l]) : 0; };
+    if (bank_aware)
+      for (int32_t g0 = 0; g0 < W; g0 += 32) {
+        const int32_t g1 = std::min(W, g0 + 32);
+        int32_t maxlen = 0;
+        for (int32_t i = g0; i < g1; ++i) {
+          const int32_t l = slot_at[(size_t)i];
+          maxlen = std::max(maxlen, rlen(l) + (int32_t)lists[(size_t)l].size());
+        }
+        for (int32_t j = 0; j < maxlen; ++j)
+          for (int32_t h = g0; h < g1; h += 16) {
+            const int32_t h1 = std::min(g1, h + 16);
             uint32_t usedv = 0, usedr = 0;
-            for (int32_t l = h; l < std::min(w1, h + 16); ++l) {
+            for (int32_t i = h; i < h1; ++i) {
+              const int32_t l = slot_at[(size_t)i];
+              if (j < rlen(l)) {
+                const int32_t k = start[l] + j;
+                usedv |= 1u << ((k + vb) & 15);
+                usedr |= 1u << (lcol[k] & 15);
+              }
+            }
+            for (int32_t i = h; i < h1; ++i) {
+              const int32_t l = slot_at[(size_t)i];
               auto& L = lists[(size_t)l];
-              if (L.size() <= j) continue;
-              size_t best = j;
+              const int32_t jj = j - rlen(l);
+              if (jj < 0 || jj >= (int32_t)L.size()) continue;
+              size_t best = (size_t)jj;
               int bestscore = -1;
-              for (size_t q = j; q < L.size(); ++q) {
+              for (size_t q = (size_t)jj; q < L.size(); ++q) {
                 const uint32_t bv = (uint32_t)(((L[q] & 0xffffu) + vb) & 15), br = (L[q] >> 16) & 15;
                 const int sc = (((usedv >> bv) & 1) ? 0 : 2) + (((usedr >> br) & 1) ? 0 : 1);
                 if (sc > bestscore) { bestscore = sc; best = q; if (sc == 3) break; }
               }
-              std::swap(L[j], L[best]);
-              usedv |= 1u << (((L[j] & 0xffffu) + vb) & 15);
-              usedr |= 1u << ((L[j] >> 16) & 15);
+              std::swap(L[(size_t)jj], L[best]);
+              usedv |= 1u << (((L[(size_t)jj] & 0xffffu) + vb) & 15);
+              usedr |= 1u << ((L[(size_t)jj] >> 16) & 15);
             }
           }
       }
     int32_t pos = 0;
-    for (int32_t l = 0; l < W; ++l) {
-      tptr[l] = (uint16_t)pos;
-      for (uint32_t q : lists[(size_t)l]) tcsc[pos++] = q;
+    for (int32_t i = 0; i < W; ++i) {
+      tptr[i] = (uint16_t)pos;
+      for (uint32_t q : lists[(size_t)slot_at[(size_t)i]]) tcsc[pos++] = q;
     }
     tptr[W] = (uint16_t)pos;
   }
@@ -387,17 +478,35 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     desc.swap(d2);
     blocks.swap(bl2);
   }
-  const int32_t ntl = (int32_t)desc.size();
+  H.desc.swap(desc);
+  H.blocks.swap(blocks);
+  H.slot_tgt.swap(slot_tgt);
+  H.slots.swap(slots);
+  H.in_ptr.swap(in_ptr);
+  H.runs.swap(runs);
+  H.nsp = nsp;
+  H.block_cap = block_cap;
+  H.window_cap = window_cap;
+  H.nnz_cap = nnz_cap;
+  return SYMM_OK;
+}
+
+int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t t_end) {
+  TiledHost H;
+  if (int rc = build_tiled_host(S, t_begin, t_end, H)) return rc;
+  const int32_t n = S.n;
+  const int64_t nsp = H.nsp;
+  const int32_t ntl = (int32_t)H.desc.size();
   TileDesc* d_desc;
   unsigned char* d_blocks;
   double* d_spill;
   int32_t *d_targets, *d_slots;
   SpillRun* d_runs;
   int rc;
-  if ((rc = upload(P, &d_desc, desc.data(), desc.size())) || (rc = upload(P, &d_blocks, blocks.data(), blocks.size())) ||
-      (rc = upload(P, &d_targets, slot_tgt.data(), slot_tgt.size())) ||
-      (rc = upload(P, &d_slots, slots.data(), slots.size())) || (rc = upload(P, &d_runs, runs.data(), runs.size())) ||
-      (rc = upload(P, &P->d_in_ptr, in_ptr.data(), in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
+  if ((rc = upload(P, &d_desc, H.desc.data(), H.desc.size())) || (rc = upload(P, &d_blocks, H.blocks.data(), H.blocks.size())) ||
+      (rc = upload(P, &d_targets, H.slot_tgt.data(), H.slot_tgt.size())) ||
+      (rc = upload(P, &d_slots, H.slots.data(), H.slots.size())) || (rc = upload(P, &d_runs, H.runs.data(), H.runs.size())) ||
+      (rc = upload(P, &P->d_in_ptr, H.in_ptr.data(), H.in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
     return rc;
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
@@ -408,9 +517,9 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   A.runs = d_runs;
   A.spill_buf = d_spill;
   A.check_n = n;
-  A.block_cap = block_cap;
-  A.window_cap = window_cap;
-  A.nnz_cap = nnz_cap;
+  A.block_cap = H.block_cap;
+  A.window_cap = H.window_cap;
+  A.nnz_cap = H.nnz_cap;
   if (const char* dbg = std::getenv("SYMM_DEBUG_SKIP")) A.debug_skip = std::atoi(dbg);  // diagnostics only
   P->fargs = FixupArgs{n, P->d_in_ptr, d_spill};
   int stages = 0;
@@ -1048,6 +1157,25 @@ extern "C" int symm_cs_format_dump(const race_schedule_t* s, int32_t wcap, int32
   if (chunk_off) std::memcpy(chunk_off, H.chunk_off.data(), H.chunk_off.size() * sizeof(int64_t));
   if (chunk_len) std::memcpy(chunk_len, H.chunk_len.data(), H.chunk_len.size() * sizeof(int32_t));
   if (blocks) std::memcpy(blocks, H.blocks.data(), H.blocks.size());
+  return SYMM_OK;
+}
+
+// Diagnostics / CPU tests: the K3/K4 tile blocks exactly as the plan would
+// upload them (whole schedule, one rank).  sizes = {tiles, block bytes,
+// runs, spill slots}; any output pointer may be NULL (sizes only).
+extern "C" int symm_tiled_format_dump(const race_schedule_t* s, int64_t* sizes, void* desc, unsigned char* blocks,
+                                      void* runs, int32_t* targets) {
+  if (!s || !sizes) return set_error(SYMM_ERR_ARG, "NULL argument");
+  TiledHost H;
+  if (int rc = build_tiled_host(s->S, 0, (int32_t)s->S.tile_group.size(), H)) return rc;
+  sizes[0] = (int64_t)H.desc.size();
+  sizes[1] = (int64_t)H.blocks.size();
+  sizes[2] = (int64_t)H.runs.size();
+  sizes[3] = (int64_t)H.slot_tgt.size();
+  if (desc) std::memcpy(desc, H.desc.data(), H.desc.size() * sizeof(TileDesc));
+  if (blocks) std::memcpy(blocks, H.blocks.data(), H.blocks.size());
+  if (runs) std::memcpy(runs, H.runs.data(), H.runs.size() * sizeof(SpillRun));
+  if (targets) std::memcpy(targets, H.slot_tgt.data(), H.slot_tgt.size() * sizeof(int32_t));
   return SYMM_OK;
 }
 

@@ -69,12 +69,16 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
 //   TileDesc (64 B) | start u16[T+1] | lcol u16[nnz] | tcsc u32[noff] |
-//   tptr u16[W+1] | tgt i32[S] | val f64[nnz]
+//   tptr u16[W+1] | [sid u16[W]] | tgt i32[S] | val f64[nnz]
 // start: entry offsets of the T own rows (natural row order); lcol: local
 // column of each entry (own rows 0..T-1, then spill targets T..W-1);
 // tcsc/tptr: the off-diagonal entries grouped by local target (CSC of the
-// tile), each as (entry index | local row << 16); tgt: global row of each
-// spill target.  K3's staging slots live outside the block (`slots`).
+// tile), each as (entry index | local row << 16), one list per lane
+// position i (tptr[i] .. tptr[i+1]); sid (sorted tiles only): the window
+// slot of lane position i, positions sorted by descending work (row entries
+// + transposed entries) so the lanes of a warp have similar list lengths;
+// unsorted tiles: position i is slot i.  tgt: global row of each spill
+// target.  K3's staging slots live outside the block (`slots`).
 struct TileDesc {
   int64_t block_off;    // byte offset of the block
   int32_t block_bytes;  // multiple of 16, < 65536
@@ -85,13 +89,14 @@ struct TileDesc {
                         // have target -1
   int32_t nnz;          // stored entries of the tile
   int32_t row0;         // first own row (permuted id)
-  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_slot, o_val;  // byte offsets in the block (o_slot unused)
+  uint16_t o_lcol, o_tidx, o_tptr, o_tgt, o_sid, o_val;  // byte offsets in the block
   int32_t spill_off;    // first spill slot of this tile (targets / slots arrays)
   int32_t run_off;      // first run of this tile (runs array)
   int32_t nruns;        // runs of consecutive spill targets
   int32_t gather_runs;  // 1: the gather warps bulk-copy the runs (long runs); 0: they
                         // cp.async slot by slot from the block's tgt list (short runs)
-  int32_t pad[2];
+  int32_t sorted;       // 1: lanes take the window slots in the order sid[] (work-sorted)
+  int32_t pad;
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
 

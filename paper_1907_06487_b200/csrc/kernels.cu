@@ -482,27 +482,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
     const uint32_t* tcsc = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
+    const uint16_t* sid = reinterpret_cast<const uint16_t*>(blk + D.o_sid);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
     const int32_t* slot = A.slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
-    // one pass, one thread per local target l (fixed order -> deterministic):
-    //   own row l:  sum_{e in row l} a_e x[c_e]                    (PAPER.md:738-739, tmp)
-    //   every l:    sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
-    for (int l = gt; l < W; l += kGroupThreads) {
-      // K3: the staging slot is fetched first so its latency overlaps the sums
-      const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
-      double acc = 0.0;
-      if (l < T && !(A.debug_skip & 1)) {
-        const int eb = start[l], ee = start[l + 1];
-#pragma unroll 4
-        for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
-      }
-      const int jb = tptr[l], je = (A.debug_skip & 2) ? jb : tptr[l + 1];
-#pragma unroll 4
-      for (int j = jb; j < je; ++j) {
-        const uint32_t q = tcsc[j];
-        acc += val[q & 0xffffu] * xs[q >> 16];
-      }
+    // flush of window slot l: K4 one RED per (tile, target); K3 own rows
+    // stored, spill contributions staged
+    auto flush = [&](int l, int sl, double acc) {
       if (A.debug_skip & 4) {
         // diagnostics: no flush
       } else if (ATOMIC) {
@@ -515,6 +501,56 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         y[row0 + l] = acc;
       } else if (sl >= 0) {
         __stcg(A.spill_buf + sl, acc);
+      }
+    };
+    // one thread per window slot (fixed summation order per slot ->
+    // deterministic):
+    //   own row l:  sum_{e in row l} a_e x[c_e]                    (PAPER.md:738-739, tmp)
+    //   then:       sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
+    if (!D.sorted) {
+      // slot order: a warp walks the row parts of 32 consecutive slots in
+      // lock step, then their transposed parts
+      for (int l = gt; l < W; l += kGroupThreads) {
+        // K3: the staging slot is fetched first so its latency overlaps the sums
+        const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
+        double acc = 0.0;
+        if (l < T && !(A.debug_skip & 1)) {
+          const int eb = start[l], ee = start[l + 1];
+#pragma unroll 4
+          for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
+        }
+        const int jb = tptr[l], je = (A.debug_skip & 2) ? jb : tptr[l + 1];
+#pragma unroll 4
+        for (int j = jb; j < je; ++j) {
+          const uint32_t q = tcsc[j];
+          acc += val[q & 0xffffu] * xs[q >> 16];
+        }
+        flush(l, sl, acc);
+      }
+    } else {
+      // work-sorted: lane position i takes slot sid[i] and walks one list,
+      // its row part then its transposed part (the lanes of a warp have
+      // similar total lengths)
+      for (int i = gt; i < W; i += kGroupThreads) {
+        const int l = sid[i];
+        const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
+        int eb = 0, nr = 0;
+        if (l < T && !(A.debug_skip & 1)) {
+          eb = start[l];
+          nr = start[l + 1] - eb;
+        }
+        const int jb = tptr[i];
+        const int nt = nr + ((A.debug_skip & 2) ? 0 : tptr[i + 1] - jb);
+        const int jo = jb - nr;  // list position u >= nr is tcsc[jo + u]
+        double acc = 0.0;
+#pragma unroll 4
+        for (int u = 0; u < nt; ++u) {
+          uint32_t q;
+          if (u < nr) q = (uint32_t)(eb + u) | ((uint32_t)lcol[eb + u] << 16);
+          else q = tcsc[jo + u];
+          acc += val[q & 0xffffu] * xs[q >> 16];
+        }
+        flush(l, sl, acc);
       }
     }
     if (gt == 0) TRACE(k, 4);
