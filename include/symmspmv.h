@@ -76,7 +76,10 @@ typedef struct {
   int32_t max_tile_rows;    /* hard cap on rows per tile (<= 65535)                          */
   int32_t max_tile_window;  /* cap on |own rows ∪ targets| per tile (smem entries)           */
   int32_t max_tile_nnz;     /* cap on stored entries per tile (smem staging of the tile)     */
-  int32_t reorder;          /* 1 = BFS level permutation; 0 = keep order */
+  int32_t reorder;          /* 1 = BFS level permutation; 2 = RCM levels
+                               (Cuthill-McKee within-level order, whole order reversed,
+                               PAPER.md:1052-1053, 2026, 2047; needs cone_tiles = 0);
+                               0 = keep order */
   int32_t cone_tiles;       /* 0 = contiguous tiles (default); 1/2 = tiles are cones across the
                                levels of their level group (1: proportional cuts, 2: cuts
                                follow BFS discovery), rows re-permuted inside the group */

@@ -225,3 +225,34 @@ def nrows_eff(node):
 def eta(nrows_total, root, nthreads: int) -> float:
     """η = nrows_total / (nrowsEff(T_{-1}(0)) × nthreads), PAPER.md:1803-1812."""
     return float(nrows_total) / (float(nrows_eff(root)) * float(nthreads))
+
+
+def rcm_order(g_ptr, g_adj, roots):
+    """Reverse Cuthill-McKee order (PAPER.md:1052-1053 names RCM as RACE's
+    alternative level construction; PAPER.md:2026, 2047, 2199 use it).
+    Cuthill-McKee: a BFS from each root in turn (one per connected component,
+    in the given order) that appends the unvisited neighbours of the vertex
+    being expanded by ascending degree, ties by ascending index; the reverse
+    of the whole visit order is RCM.  Returns the RCM order (position ->
+    vertex) as a list.  Pure Python, for test-sized graphs."""
+    n = len(g_ptr) - 1
+    deg = [int(g_ptr[v + 1]) - int(g_ptr[v]) for v in range(n)]
+    seen = [False] * n
+    order = []
+    for r in roots:
+        r = int(r)
+        if seen[r]:
+            continue
+        seen[r] = True
+        queue = [r]
+        head = 0
+        while head < len(queue):
+            u = queue[head]
+            head += 1
+            new = [int(v) for v in g_adj[int(g_ptr[u]):int(g_ptr[u + 1])] if not seen[int(v)]]
+            new = sorted(set(new), key=lambda v: (deg[v], v))
+            for v in new:
+                seen[v] = True
+                queue.append(v)
+        order.extend(queue)
+    return order[::-1]

@@ -352,7 +352,8 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   if (cfg.k < 2) return set_error(SYMM_ERR_K, "distance k = %d < 2: SymmSpMV needs distance-2 (PAPER.md:787-789)", cfg.k);
   if (cfg.tile_work <= 0 || cfg.max_tile_rows <= 0 || cfg.max_tile_rows > 65535 || cfg.max_tile_window < 64 ||
       cfg.max_tile_window > 65535 || cfg.max_tile_nnz < 1 || cfg.max_tile_nnz > 65535 || cfg.n_eps < 1 || cfg.n_eps > 8 || cfg.n_workers < 0 ||
-      cfg.scheme < 0 || cfg.scheme > 2 || (cfg.scheme == 2 && cfg.abmc_block < 1))
+      cfg.scheme < 0 || cfg.scheme > 2 || (cfg.scheme == 2 && cfg.abmc_block < 1) || cfg.reorder < 0 ||
+      cfg.reorder > 2 || (cfg.reorder == 2 && cfg.cone_tiles))
     return set_error(SYMM_ERR_ARG, "invalid race_config field");
   int rc = validate_upper(U);
   if (rc) return rc;
@@ -397,10 +398,16 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
         for (size_t q = lvl_begin; q < lvl_end; ++q) {
           int32_t u = order[q];
           disc[q] = (int32_t)order.size();
+          const size_t c0 = order.size();
           for (int64_t e = gp[(size_t)u]; e < gp[(size_t)u + 1]; ++e) {
             int32_t j = ga[(size_t)e];
             if (S->dist[(size_t)j] == -1) { S->dist[(size_t)j] = lvl + 1; order.push_back(j); }
           }
+          if (cfg.reorder == 2)  // Cuthill-McKee: u's new neighbours by ascending degree, then index
+            std::sort(order.begin() + (int64_t)c0, order.end(), [&](int32_t a, int32_t b) {
+              const int64_t da = gp[(size_t)a + 1] - gp[(size_t)a], db = gp[(size_t)b + 1] - gp[(size_t)b];
+              return da != db ? da < db : a < b;
+            });
         }
         lvl_begin = lvl_end;
         lvl_end = order.size();
@@ -408,6 +415,13 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
       }
     }
     const int32_t totalLvl = maxLvl + 1;
+    if (cfg.reorder == 2) {
+      // Reverse Cuthill-McKee: the whole CM
+      // order reversed; levels stay contiguous, relabelled from the far end
+      // (island separators stay empty levels)
+      std::reverse(order.begin(), order.end());
+      for (int32_t v = 0; v < n; ++v) S->dist[(size_t)v] = maxLvl - S->dist[(size_t)v];
+    }
     S->level_ptr.assign((size_t)std::max(totalLvl, 0) + 1, 0);
     if (cfg.reorder) {
       for (int32_t v = 0; v < n; ++v) S->level_ptr[(size_t)S->dist[(size_t)v] + 1] += 1;

@@ -215,3 +215,14 @@ def test_mc_abmc_schedules(scheme, block, variant):
     y_ref = oracle.symmspmv(U, x)
     outs, _, _ = run_gpu(U, x, variant, sched_kw=dict(scheme=scheme, abmc_block=block))
     assert relinf(outs[0], y_ref) <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["st27_24", "fem_knn_30k", "spin_14"])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_rcm_schedule(name, variant):
+    """NEXT-2: RCM level construction (reorder = 2) runs through every kernel."""
+    U, x = gen.make_config(name)
+    y_ref = oracle.symmspmv(U, x)
+    outs, _, _ = run_gpu(U, x, variant, sched_kw=dict(reorder=2))
+    assert relinf(outs[0], y_ref) <= TOL

@@ -246,3 +246,39 @@ def test_distk_bruteforce_path():
         expect = int(np.sum((D <= k) & (D > 0) & (bad[:, None] == bad[None, :])))
         got = oracle.distk_violations(gp, ga, k, bad)
         assert got == expect and got > 0
+
+
+# ------------------------------------------------------------------ RCM pins
+def test_rcm_textbook_cases():
+    """Cuthill-McKee by hand: a path from an end is the
+    natural order (RCM its reverse); a star from a leaf visits the centre,
+    then the other leaves by index; children go by ascending degree."""
+    from oracle.race import rcm_order
+    gp, ga = oracle.graph(gen.path(6))
+    assert rcm_order(gp, ga, [0]) == [5, 4, 3, 2, 1, 0]
+    star = gen.from_edges(6, [0] * 5, [1, 2, 3, 4, 5])
+    gp, ga = oracle.graph(star)
+    assert rcm_order(gp, ga, [3]) == [5, 4, 2, 1, 0, 3]
+    # root 0 with neighbours 1 (degree 3), 2 (degree 1), 3 (degree 2)
+    U = gen.from_edges(6, [0, 0, 0, 1, 1, 3], [1, 2, 3, 4, 5, 4])
+    gp, ga = oracle.graph(U)
+    assert rcm_order(gp, ga, [0])[::-1][:4] == [0, 2, 3, 1]
+
+
+@pytest.mark.parametrize("mk", [lambda: gen.lap2d(9), lambda: gen.knn(300, 6, 3), lambda: gen.st27(5, 2, True),
+                                lambda: gen.random_symmetric(200, 6.0, 1)])
+def test_rcm_vs_scipy(mk):
+    """On a connected graph scipy's reverse_cuthill_mckee starts from a
+    minimum-degree vertex (its choice among ties is its own) and orders
+    children by degree, ties by index; the oracle from scipy's start vertex
+    (the last vertex of its RCM order) must give the identical order."""
+    from oracle.race import rcm_order
+    U = mk()
+    gp, ga = oracle.graph(U)
+    A = sp.csr_matrix((np.ones(len(ga)), ga, gp), shape=(U.n, U.n))
+    ncomp, _ = csg.connected_components(A, directed=False)
+    assert ncomp == 1
+    ref = csg.reverse_cuthill_mckee(A, symmetric_mode=True)
+    root = int(ref[-1])
+    assert np.diff(gp)[root] == np.diff(gp).min()
+    assert rcm_order(gp, ga, [root]) == list(ref)

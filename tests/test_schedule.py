@@ -238,3 +238,30 @@ def test_degenerate_inputs():
     U = gen.from_edges(n, [0] * (n - 1), list(range(1, n)), has_diag=(np.arange(n) % 3 != 0).astype(np.int8))
     s = P.build_schedule(U, tile_work=20)
     _check_schedule_bruteforce(U, s)
+
+
+@pytest.mark.parametrize("name,mk", GRAPHS)
+def test_rcm_levels_match_oracle(name, mk):
+    """reorder = 2: the permutation is the oracle's reverse Cuthill-McKee order
+    from the builder's roots; levels are the
+    BFS levels of Eq. 5 counted from the far end, contiguous and ascending."""
+    from oracle.race import rcm_order
+    U = mk()
+    s = P.build_schedule(U, reorder=2)
+    roots = s.table("roots")
+    gp, ga = oracle.graph(U)
+    perm, inv = s.permutation()
+    assert list(inv) == rcm_order(gp, ga, roots)
+    d_or, tl = oracle.bfs_levels(gp, ga, roots)
+    dist = s.table("dist")
+    assert np.array_equal(dist, (tl - 1) - d_or)
+    assert np.all(np.diff(dist[inv]) >= 0)
+    assert np.array_equal(np.diff(s.table("level_ptr")), _levels_from_dist(dist))
+    # the schedule is still conflict free and the permuted matrix is P A P^T
+    rp, col, val = s.permuted_matrix()
+    x = gen.vector_uniform(U.n, 3)
+    yp = oracle.symmspmv(gen.UpperCSR(U.n, rp, col, val), x[inv])
+    y = oracle.symmspmv(U, x)
+    assert np.max(np.abs(yp - y[inv])) <= 1e-13 * max(1.0, np.max(np.abs(y)))
+    with pytest.raises(Exception):
+        P.build_schedule(U, reorder=2, cone_tiles=1)
