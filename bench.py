@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="st27_128")
-    ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "auto"])
+    ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "tree", "auto"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-variants", action="store_true", help="also time the other variants (extra key)")

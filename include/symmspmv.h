@@ -87,6 +87,11 @@ typedef struct {
   int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
   uint32_t flags;           /* bit 0: within-level order = original index (experimental)    */
   int32_t scheme;           /* 0 = RACE (levels, groups, tiles: the default);
+                               3 = RACE with the recursive tree (§4.4.1-4.4.2):
+                                   level groups with > 1 worker refined stage by stage on their
+                                   distance-1-extended subgraphs; leaves become the level groups;
+                                   workers = n_workers (0: 8 x 148); needs reorder >= 1,
+                                   cone_tiles = 0; run by the `tree` variant (or any other);
                                1 = MC: greedy distance-2 (write-set) colouring of single rows,
                                    rows ordered colour by colour;
                                2 = ABMC: blocks of `abmc_block` consecutive BFS-ordered rows,
@@ -159,9 +164,15 @@ typedef enum {
   SYMM_VARIANT_COLORED_SMEM = 5,/* K5: RACE write-set colours run inside a shared-memory x/y window
                                    (plain smem read-modify-write, one barrier per colour); window
                                    flushed with fp64 RED into zeroed y                        */
-  SYMM_VARIANT_SPMV = 6         /* the paper's yardstick (Alg. 1): the same y := A x
+  SYMM_VARIANT_SPMV = 6,        /* the paper's yardstick (Alg. 1): the same y := A x
                                    from the FULL matrix A = U + U^T - diag(U) in CRS, the plan
                                    mirrors U; deterministic, no atomics   */
+  SYMM_VARIANT_TREE = 7         /* K7: the recursive RACE tree (schedule scheme 3 only, else
+                                   SYMM_ERR_ARG) in one persistent launch: one CTA per leaf at a
+                                   time, leaves claimed in red-before-blue depth-first order,
+                                   tree-scoped sync through per-node counters (a blue child waits
+                                   for the leaves of its red siblings),
+                                   plain read-modify-write of y as in COLORED; deterministic    */
 } symm_variant;
 
 typedef enum { SYMM_ORDER_PERMUTED = 0, SYMM_ORDER_ORIGINAL = 1 } symm_vec_order;

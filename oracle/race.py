@@ -256,3 +256,97 @@ def rcm_order(g_ptr, g_adj, roots):
                 queue.append(v)
         order.extend(queue)
     return order[::-1]
+
+
+def race_tree(g_ptr, g_adj, inv, groups, nthreads: int, k: int, eps_list):
+    """The recursive RACE tree (§4.4.1-4.4.2), step by step.
+
+    inv: position -> vertex after the stage-0 level permutation; groups: the
+    stage-0 level groups T_0(j) as (first position, end position, workers).
+    A level group T_s(j) with more than one worker is refined: (1) levels are
+    constructed on the subgraph of T_s(j) plus its distance-1 neighbourhood
+    (distance-(k-1) for k = 2), one BFS per island in the
+    group's current order (root = its first unvisited group vertex, reading
+    R29), a new island starting two levels further (PAPER.md:1406-1411);
+    (2) only the vertices of T_s(j) are kept in the new levels L_{s+1}
+     and the group is re-permuted in that order
+    (PAPER.md:1489-1491); (3) eps_{s+1} aggregation (PAPER.md:1567-1625) of
+    the new levels with the group's workers (rows as the workload, reading
+    R30), the red/blue split and Alg. 4 give T_{s+1}(:).  A group that yields
+    fewer than two non-empty level groups stays a leaf (reading R31).
+    Returns (nodes, inv): nodes[i] = (parent, child index, first, end, stage,
+    workers), node 0 = T_{-1}(0), children listed after their parent."""
+    inv = [int(v) for v in inv]
+    n = len(inv)
+    nodes = [(-1, 0, 0, n, -1, int(nthreads))]
+    for j, (a, b, w) in enumerate(groups):
+        nodes.append((0, j, int(a), int(b), 0, int(w)))
+    i = 1
+    while i < len(nodes):
+        _, _, p0, p1, st0, w = nodes[i]
+        node_id, i = i, i + 1
+        st = st0 + 1
+        if w <= 1 or p1 - p0 < 2:
+            continue
+        G = set(inv[p0:p1])
+        H = set(G)
+        for v in inv[p0:p1]:
+            H.update(int(u) for u in g_adj[int(g_ptr[v]):int(g_ptr[v + 1])])
+        level = {}
+        bfs = []
+        maxL = -1
+        for root in inv[p0:p1]:               # (1) one BFS per island
+            if root in level:
+                continue
+            level[root] = 0 if maxL < 0 else maxL + 2
+            queue = [root]
+            h = 0
+            while h < len(queue):
+                u = queue[h]
+                h += 1
+                maxL = max(maxL, level[u])
+                for v in g_adj[int(g_ptr[u]):int(g_ptr[u + 1])]:
+                    v = int(v)
+                    if v in H and v not in level:
+                        level[v] = level[u] + 1
+                        queue.append(v)
+            bfs.extend(queue)
+        keep = [v for v in bfs if v in G]    # (2) the group's own vertices
+        lw = [0] * (maxL + 1)
+        for v in keep:
+            lw[level[v]] += 1
+        eps = eps_list[min(st, len(eps_list) - 1)]
+        wins = eps_aggregate(lw, w, k, eps)  # (3)
+        T, wk = [], []
+        if wins:
+            T.append(wins[0][0])
+        for (f, e, b) in wins:
+            T += [split_window(lw, f, e, k), e]
+            wk += [b, b]
+        if len(T) >= 3:
+            T, _ = alg4_balance(T, wk, lw, kmin=k)
+        inv[p0:p1] = keep
+        sizes = [sum(lw[T[j]:T[j + 1]]) for j in range(len(T) - 1)]
+        if sum(1 for c in sizes if c > 0) < 2:
+            continue
+        a = p0
+        for j, c in enumerate(sizes):
+            nodes.append((node_id, j, a, a + c, st, wk[j]))
+            a += c
+    return nodes, inv
+
+
+def tree_eta(nodes, nthreads: int) -> float:
+    """§5 eta of a tree given as race_tree's node list (rows as the workload):
+    nested lists of children for nrows_eff."""
+    kids = {i: [] for i in range(len(nodes))}
+    for i, nd in enumerate(nodes[1:], start=1):
+        kids[nd[0]].append(i)
+
+    def build(i):
+        if not kids[i]:
+            return nodes[i][3] - nodes[i][2]
+        ch = sorted(kids[i], key=lambda c: nodes[c][1])
+        return [build(c) for c in ch]
+
+    return eta(nodes[0][3] - nodes[0][2], build(0), nthreads)

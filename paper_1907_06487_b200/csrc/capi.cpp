@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -60,6 +61,10 @@ struct symmspmv_plan {
   int tiled_occ = 0;
   int32_t* d_in_ptr = nullptr;
   FixupArgs fargs{};
+  // K7 recursive tree
+  bool has_tree = false;
+  TreeArgs tree{};
+  int tree_grid = 0;
   // K6 full-matrix SpMV (yardstick)
   bool has_spmv = false;
   int32_t *d_frp = nullptr, *d_fcol = nullptr;
@@ -660,6 +665,78 @@ int build_colored(symmspmv_plan_t* P, const Schedule& S) {
   return SYMM_OK;
 }
 
+// K7: the recursive tree's leaves in execution order (depth first, red
+// children before blue children), per leaf its tiles, the ancestors it waits
+// at (it lies in a blue child) and the ancestors it counts at (red child).
+int build_tree(symmspmv_plan_t* P, const Schedule& S) {
+  const int32_t nn = (int32_t)S.tree_parent.size();
+  if (nn == 0) return set_error(SYMM_ERR_ARG, "variant TREE needs a schedule built with scheme = 3 (recursive tree)");
+  std::vector<std::vector<int32_t>> kids((size_t)nn);
+  for (int32_t v = 1; v < nn; ++v) kids[(size_t)S.tree_parent[(size_t)v]].push_back(v);
+  for (auto& k : kids)
+    std::sort(k.begin(), k.end(), [&](int32_t a, int32_t b) { return S.tree_cidx[(size_t)a] < S.tree_cidx[(size_t)b]; });
+  std::vector<int32_t> group_of_node((size_t)nn, -1);
+  for (size_t g = 0; g < S.tree_leaf.size(); ++g) group_of_node[(size_t)S.tree_leaf[g]] = (int32_t)g;
+  const int32_t ng = (int32_t)S.tree_leaf.size(), nt = (int32_t)S.tile_group.size();
+  std::vector<int32_t> gt0((size_t)ng, nt), gt1((size_t)ng, 0);
+  for (int32_t t = 0; t < nt; ++t) {
+    const int32_t g = S.tile_group[(size_t)t];
+    gt0[(size_t)g] = std::min(gt0[(size_t)g], t);
+    gt1[(size_t)g] = std::max(gt1[(size_t)g], t + 1);
+  }
+  std::vector<int32_t> order;  // execution order of the leaves (node ids)
+  std::vector<int32_t> red_total((size_t)nn, 0);
+  std::function<int32_t(int32_t)> visit = [&](int32_t v) -> int32_t {  // returns leaves under v
+    if (kids[(size_t)v].empty()) {
+      if (group_of_node[(size_t)v] < 0) return 0;  // empty node
+      order.push_back(v);
+      return 1;
+    }
+    int32_t red = 0, tot = 0;
+    for (int par = 0; par < 2; ++par)
+      for (int32_t c : kids[(size_t)v])
+        if ((S.tree_cidx[(size_t)c] & 1) == par) {
+          const int32_t k = visit(c);
+          if (par == 0) red += k;
+          tot += k;
+        }
+    red_total[(size_t)v] = red;
+    return tot;
+  };
+  visit(0);
+  const int32_t nl = (int32_t)order.size();
+  std::vector<int32_t> t0((size_t)nl), t1((size_t)nl), wptr(1, 0), wnode, sptr(1, 0), snode;
+  for (int32_t i = 0; i < nl; ++i) {
+    const int32_t g = group_of_node[(size_t)order[(size_t)i]];
+    t0[(size_t)i] = gt0[(size_t)g];
+    t1[(size_t)i] = std::max(gt0[(size_t)g], gt1[(size_t)g]);
+    for (int32_t v = order[(size_t)i]; S.tree_parent[(size_t)v] >= 0; v = S.tree_parent[(size_t)v]) {
+      const int32_t a = S.tree_parent[(size_t)v];
+      if (S.tree_cidx[(size_t)v] & 1) {
+        if (red_total[(size_t)a] > 0) wnode.push_back(a);
+      } else {
+        snode.push_back(a);
+      }
+    }
+    wptr.push_back((int32_t)wnode.size());
+    sptr.push_back((int32_t)snode.size());
+  }
+  if (wnode.empty()) wnode.push_back(0);
+  if (snode.empty()) snode.push_back(0);
+  int32_t *d_t0, *d_t1, *d_wp, *d_wn, *d_sp, *d_sn, *d_rt, *d_cnt;
+  int rc;
+  if ((rc = upload(P, &d_t0, t0.data(), t0.size())) || (rc = upload(P, &d_t1, t1.data(), t1.size())) ||
+      (rc = upload(P, &d_wp, wptr.data(), wptr.size())) || (rc = upload(P, &d_wn, wnode.data(), wnode.size())) ||
+      (rc = upload(P, &d_sp, sptr.data(), sptr.size())) || (rc = upload(P, &d_sn, snode.data(), snode.size())) ||
+      (rc = upload(P, &d_rt, red_total.data(), red_total.size())) || (rc = dev_alloc(P, &d_cnt, (size_t)nn + 1)))
+    return rc;
+  P->tree = TreeArgs{nl, nn, d_t0, d_t1, d_wp, d_wn, d_sp, d_sn, d_rt, d_cnt};
+  // one resident CTA per worker of the tree (256 threads: 8 per SM)
+  P->tree_grid = std::max(1, std::min(nl, 8 * P->sms));
+  P->has_tree = true;
+  return SYMM_OK;
+}
+
 int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cudaStream_t st) {
   int rc = 0;
   P->last_launches = 0;
@@ -696,6 +773,15 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
     if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, true, st)))
       return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
+    P->last_launches = 2;
+  } else if (variant == SYMM_VARIANT_TREE) {
+    if (!P->has_tree) return set_error(SYMM_ERR_ARG, "variant TREE was not uploaded by this plan");
+    CsrArgs A{P->n, P->d_rp, P->d_col, P->d_val};
+    ColoredArgs C{P->d_tile_ptr, P->d_phase_tiles, 0, P->d_srow, P->d_tile_sub_ptr, P->d_sub_ptr};
+    cudaError_t e = cudaMemsetAsync(P->tree.counters, 0, sizeof(int32_t) * ((size_t)P->tree.nnodes + 1), st);
+    if (e != cudaSuccess) return cuda_fail(e, "tree counters");
+    if ((rc = launch_zero(y, P->n, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    if ((rc = launch_tree(A, C, P->tree, x, y, P->vec, P->tree_grid, st))) return cuda_fail((cudaError_t)rc, "k_tree");
     P->last_launches = 2;
   } else if (variant == SYMM_VARIANT_SPMV) {
     if (!P->has_spmv) return set_error(SYMM_ERR_ARG, "variant SPMV was not uploaded by this plan");
@@ -830,6 +916,13 @@ int race_schedule_table(const race_schedule_t* s, const char* which, int64_t* le
   else if (w == "tile_sub_ptr") v = &S.tile_sub_ptr;
   else if (w == "sub_ptr") v = &S.sub_ptr;
   else if (w == "spill") v = &S.spill;
+  else if (w == "tree_parent") v = &S.tree_parent;
+  else if (w == "tree_cidx") v = &S.tree_cidx;
+  else if (w == "tree_r0") v = &S.tree_r0;
+  else if (w == "tree_r1") v = &S.tree_r1;
+  else if (w == "tree_stage") v = &S.tree_stage;
+  else if (w == "tree_workers") v = &S.tree_workers;
+  else if (w == "tree_leaf") v = &S.tree_leaf;
   else if (w == "own_first") {
     *len = (int64_t)S.own_first.size();
     if (out) for (size_t i = 0; i < S.own_first.size(); ++i) out[i] = S.own_first[i];
@@ -881,7 +974,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   if (U && (U->n != S.n || U->nnz != S.nnz))
     return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
                      (long long)U->nnz, S.n, (long long)S.nnz);
-  if (opt.variant < 0 || opt.variant > 6) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
+  if (opt.variant < 0 || opt.variant > 7) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
   if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks)
     return set_error(SYMM_ERR_ARG, "rank %d of %d", opt.rank, opt.nranks);
   if (opt.nranks > 1 && opt.variant != SYMM_VARIANT_TILED_ATOMIC && opt.variant != SYMM_VARIANT_AUTO)
@@ -922,8 +1015,10 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
   bool want_cs = all || v == SYMM_VARIANT_COLORED_SMEM;
   bool want_spmv = all || v == SYMM_VARIANT_SPMV;
+  bool want_tree = (all && !S.tree_parent.empty()) || v == SYMM_VARIANT_TREE;
+  if (want_tree) want_col = want_csr = true;
   if (opt.nranks > 1) {
-    want_col = want_csr = want_cs = want_spmv = false;
+    want_col = want_csr = want_cs = want_spmv = want_tree = false;
     P->variant = SYMM_VARIANT_TILED_ATOMIC;
   }
   if (want_tiled) {
@@ -948,6 +1043,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   if (!rc && want_col) rc = build_colored(P, S);
   if (!rc && want_cs) rc = build_cs(P, S);
   if (!rc && want_spmv) rc = build_spmv(P, S);
+  if (!rc && want_tree) rc = build_tree(P, S);
   if (!rc) {
     if (!(rc = upload(P, &P->d_perm, S.perm.data(), S.perm.size())) &&
         !(rc = upload(P, &P->d_inv, S.inv.data(), S.inv.size())) && !(rc = dev_alloc(P, &P->d_xp, (size_t)S.n)))

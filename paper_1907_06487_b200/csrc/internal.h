@@ -50,6 +50,15 @@ struct Schedule {
   int64_t bw_before = 0, bw_after = 0;
   double eta = 1.0;
   double build_seconds = 0.0;
+  // NEXT-2 recursive RACE tree (race_config.scheme == 3; §4.4.1-4.4.2):
+  // node 0 = T_{-1}(0) (all rows), its children the stage-0 level groups,
+  // deeper nodes the level groups T_{s+1} found inside a T_s with > 1 worker.
+  // Rows of every node are contiguous [tree_r0, tree_r1); the children of a
+  // node alternate red (even tree_cidx) / blue (odd).  Leaves = the level
+  // groups of the final schedule (group g <-> node tree_leaf[g]).
+  std::vector<int32_t> tree_parent, tree_cidx, tree_r0, tree_r1, tree_stage, tree_workers;
+  std::vector<int32_t> tree_leaf;   // [n_groups] leaf node of every group (position order)
+  double tree_eta = 0.0;            // §5 eta of the tree (rows as the workload)
 };
 
 // Paper-algorithm building blocks (exposed for white-box tests through
@@ -141,6 +150,21 @@ struct ColoredArgs {
   const int32_t* tile_sub_ptr; // offsets into sub_ptr per tile
   const int32_t* sub_ptr;      // per tile colour pointers, relative to tile row start
 };
+
+// ---- K7 tree (scheme 3): leaves in execution order (red subtrees before blue)
+struct TreeArgs {
+  int32_t nleaves, nnodes;
+  const int32_t* leaf_t0;      // [nleaves] tiles [leaf_t0[i], leaf_t1[i]) of leaf i (execution order)
+  const int32_t* leaf_t1;
+  const int32_t* wait_ptr;     // [nleaves+1] into wait_node
+  const int32_t* wait_node;    // nodes whose red-subtree leaves leaf i waits for
+  const int32_t* sig_ptr;      // [nleaves+1] into sig_node
+  const int32_t* sig_node;     // nodes whose red-leaf counter leaf i increments
+  const int32_t* red_total;    // [nnodes] leaves under the red children of every node
+  int32_t* counters;           // [nnodes + 1]; the last one is the claim counter (zeroed per run)
+};
+int launch_tree(const CsrArgs& A, const ColoredArgs& C, const TreeArgs& T, const double* x, double* y, int vec,
+                int grid, void* stream);
 
 // ---- K5 colored_smem (cs_build.cpp / kernels.cu) ------------------------------
 // One tile = consecutive schedule tiles of one level group; rows coloured by

@@ -139,15 +139,18 @@ __global__ void __launch_bounds__(256) k_spmv(CsrArgs A, const double* __restric
 }
 
 // ---------------------------------------------------------------- K2 colored
+// One tile by one CTA: the tile's intra-tile colours one after the other
+// (__syncthreads between), V lanes per row, plain read-modify-write of y
+// through L2 (write-disjoint inside a colour and across the tiles that may
+// run at the same time).
 template <int V>
-__global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const double* __restrict__ x,
-                                                 double* __restrict__ y) {
+__device__ __forceinline__ void colored_tile(const CsrArgs& A, const ColoredArgs& C, int t,
+                                             const double* __restrict__ x, double* __restrict__ y) {
   constexpr int RPW = 32 / V;
   const int lane = threadIdx.x & 31;
   const int sub = lane % V;
   const int wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  const int t = C.phase_tiles[blockIdx.x];
   const int r0 = C.tile_ptr[t];
   const int* sp = C.sub_ptr + C.tile_sub_ptr[t];
   const int nsub = C.tile_sub_ptr[t + 1] - C.tile_sub_ptr[t] - 1;
@@ -177,6 +180,47 @@ __global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const
       if (valid && sub == 0) __stcg(y + row, __ldcg(y + row) + sum);
     }
     __syncthreads();
+  }
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) k_colored(CsrArgs A, ColoredArgs C, const double* __restrict__ x,
+                                                 double* __restrict__ y) {
+  colored_tile<V>(A, C, C.phase_tiles[blockIdx.x], x, y);
+}
+
+// ---------------------------------------------------------------- K7 tree
+// The recursive RACE tree in one persistent launch (NEXT-2).  A CTA claims
+// the next leaf in execution order (red subtrees before blue, depth first),
+// waits until, at every ancestor where the leaf lies in a blue child, all the
+// leaves under that ancestor's red children are done (tree-scoped sync of
+// PAPER.md:1418-1421), runs the leaf's tiles like K2, then counts itself at
+// every ancestor where it lies in a red child.  Every claimed leaf runs on a
+// resident CTA and waits only for leaves claimed before it: no deadlock.
+template <int V>
+__global__ void __launch_bounds__(256) k_tree(CsrArgs A, ColoredArgs C, TreeArgs T, const double* __restrict__ x,
+                                              double* __restrict__ y) {
+  __shared__ int s_leaf;
+  for (;;) {
+    if (threadIdx.x == 0) s_leaf = atomicAdd(T.counters + T.nnodes, 1);  // claim the next leaf
+    __syncthreads();
+    const int i = s_leaf;
+    if (i >= T.nleaves) break;
+    if (threadIdx.x == 0) {
+      for (int q = T.wait_ptr[i]; q < T.wait_ptr[i + 1]; ++q) {
+        const int a = T.wait_node[q];
+        const unsigned need = (unsigned)T.red_total[a];
+        while (ld_acquire_u32(reinterpret_cast<const unsigned*>(T.counters + a)) < need) __nanosleep(64);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    for (int t = T.leaf_t0[i]; t < T.leaf_t1[i]; ++t) colored_tile<V>(A, C, t, x, y);
+    // colored_tile ends with __syncthreads: every store of the leaf is issued
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int q = T.sig_ptr[i]; q < T.sig_ptr[i + 1]; ++q) atomicAdd(T.counters + T.sig_node[q], 1);
+    }
   }
 }
 
@@ -956,6 +1000,21 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
     case 8: k_colored<8><<<C.nphase_tiles, threads, 0, st>>>(A, C, x, y); break;
     case 16: k_colored<16><<<C.nphase_tiles, threads, 0, st>>>(A, C, x, y); break;
     default: k_colored<32><<<C.nphase_tiles, threads, 0, st>>>(A, C, x, y); break;
+  }
+  return (int)cudaGetLastError();
+}
+
+int launch_tree(const CsrArgs& A, const ColoredArgs& C, const TreeArgs& T, const double* x, double* y, int vec,
+                int grid, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = 256;
+  switch (vec) {
+    case 1: k_tree<1><<<grid, threads, 0, st>>>(A, C, T, x, y); break;
+    case 2: k_tree<2><<<grid, threads, 0, st>>>(A, C, T, x, y); break;
+    case 4: k_tree<4><<<grid, threads, 0, st>>>(A, C, T, x, y); break;
+    case 8: k_tree<8><<<grid, threads, 0, st>>>(A, C, T, x, y); break;
+    case 16: k_tree<16><<<grid, threads, 0, st>>>(A, C, T, x, y); break;
+    default: k_tree<32><<<grid, threads, 0, st>>>(A, C, T, x, y); break;
   }
   return (int)cudaGetLastError();
 }

@@ -352,7 +352,8 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   if (cfg.k < 2) return set_error(SYMM_ERR_K, "distance k = %d < 2: SymmSpMV needs distance-2 (PAPER.md:787-789)", cfg.k);
   if (cfg.tile_work <= 0 || cfg.max_tile_rows <= 0 || cfg.max_tile_rows > 65535 || cfg.max_tile_window < 64 ||
       cfg.max_tile_window > 65535 || cfg.max_tile_nnz < 1 || cfg.max_tile_nnz > 65535 || cfg.n_eps < 1 || cfg.n_eps > 8 || cfg.n_workers < 0 ||
-      cfg.scheme < 0 || cfg.scheme > 2 || (cfg.scheme == 2 && cfg.abmc_block < 1) || cfg.reorder < 0 ||
+      cfg.scheme < 0 || cfg.scheme > 3 || (cfg.scheme == 2 && cfg.abmc_block < 1) || cfg.reorder < 0 ||
+      (cfg.scheme == 3 && (cfg.cone_tiles || !cfg.reorder)) ||
       cfg.reorder > 2 || (cfg.reorder == 2 && cfg.cone_tiles))
     return set_error(SYMM_ERR_ARG, "invalid race_config field");
   int rc = validate_upper(U);
@@ -493,7 +494,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     S->bw_after = bwa;
   };
   build_permuted();
-  if (cfg.scheme != 0) {
+  if ((cfg.scheme == 1 || cfg.scheme == 2)) {
     // ---- NEXT-3 comparison schemes: MC colours single rows,
     // ABMC colours blocks of consecutive BFS-ordered rows; both greedy in BFS
     // order by closed neighbourhoods N[v] = {v} ∪ adj(v) -- the distance-2
@@ -563,7 +564,10 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     total_work += w;
   }
   int64_t nworkers = cfg.n_workers > 0 ? cfg.n_workers : std::max<int64_t>(1, (total_work + cfg.tile_work - 1) / cfg.tile_work);
-  if (cfg.scheme != 0) {
+  // the recursive tree (scheme 3) targets a thread count like the paper's
+  // (one worker = one CTA of the tree kernel): 8 per SM of a B200 by default
+  if (cfg.scheme == 3 && cfg.n_workers <= 0) nworkers = 8 * 148;
+  if ((cfg.scheme == 1 || cfg.scheme == 2)) {
     // MC / ABMC: every colour class is its own group, split into tiles by work
     S->group_lvl.resize((size_t)totalLvl + 1);
     for (int32_t l = 0; l <= totalLvl; ++l) S->group_lvl[(size_t)l] = l;
@@ -588,6 +592,135 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     S->group_lvl = T;
     S->group_workers = wk;
   }
+  }
+  if (cfg.scheme == 3) {
+    // ---- NEXT-2: the recursive RACE tree (§4.4.1-4.4.2) --
+    // A level group T_s(j) with more than one worker is refined: BFS levels
+    // on the subgraph of T_s(j) plus its distance-(k-1) = distance-1
+    // neighbourhood (no outside vertex can then mediate a
+    // distance-2 conflict), island rule +2, only the
+    // vertices of T_s(j) kept in the new levels L_{s+1};
+    // eps_{s+1} aggregation + Alg. 4 on them give T_{s+1}(:) inside T_s(j),
+    // whose rows are re-permuted in the new level order.
+    // Readings R29-R31: root = the first vertex of the group in
+    // its current order; workload = rows; a group that yields fewer than two
+    // level groups stays a leaf.
+    auto& TP = S->tree_parent;
+    auto& TC = S->tree_cidx;
+    auto& T0 = S->tree_r0;
+    auto& T1 = S->tree_r1;
+    auto& TS = S->tree_stage;
+    auto& TW = S->tree_workers;
+    auto add_node = [&](int32_t par, int32_t ci, int32_t a, int32_t b, int32_t st, int32_t w) {
+      TP.push_back(par); TC.push_back(ci); T0.push_back(a); T1.push_back(b); TS.push_back(st); TW.push_back(w);
+      return (int32_t)TP.size() - 1;
+    };
+    add_node(-1, 0, 0, n, -1, (int32_t)std::min<int64_t>(nworkers, INT32_MAX));
+    const int32_t ng0 = (int32_t)S->group_workers.size();
+    for (int32_t g = 0; g < ng0; ++g)
+      add_node(0, g, S->level_ptr[(size_t)S->group_lvl[(size_t)g]], S->level_ptr[(size_t)S->group_lvl[(size_t)g + 1]], 0,
+               S->group_workers[(size_t)g]);
+    std::vector<int32_t> ing((size_t)n, -1), inh((size_t)n, -1), vis((size_t)n, -1), hd((size_t)n, 0);
+    std::vector<int32_t> ord, keep;
+    for (int32_t id = 1; id < (int32_t)TP.size(); ++id) {  // TP grows while we walk it
+      const int32_t p0 = T0[(size_t)id], p1 = T1[(size_t)id], w = TW[(size_t)id], st = TS[(size_t)id] + 1;
+      if (w <= 1 || p1 - p0 < 2) continue;
+      for (int32_t q = p0; q < p1; ++q) {
+        const int32_t v = S->inv[(size_t)q];
+        ing[(size_t)v] = id;
+        inh[(size_t)v] = id;
+      }
+      for (int32_t q = p0; q < p1; ++q) {
+        const int32_t v = S->inv[(size_t)q];
+        for (int64_t e = gp[(size_t)v]; e < gp[(size_t)v + 1]; ++e) inh[(size_t)ga[(size_t)e]] = id;
+      }
+      ord.clear();
+      int32_t maxL = -1;
+      for (int32_t q = p0; q < p1; ++q) {  // one BFS per island of the subgraph
+        const int32_t root = S->inv[(size_t)q];
+        if (vis[(size_t)root] == id) continue;
+        const int32_t lvl0 = maxL < 0 ? 0 : maxL + 2;
+        size_t head = ord.size();
+        ord.push_back(root);
+        vis[(size_t)root] = id;
+        hd[(size_t)root] = lvl0;
+        while (head < ord.size()) {
+          const int32_t u = ord[head++];
+          maxL = std::max(maxL, hd[(size_t)u]);
+          for (int64_t e = gp[(size_t)u]; e < gp[(size_t)u + 1]; ++e) {
+            const int32_t v = ga[(size_t)e];
+            if (inh[(size_t)v] == id && vis[(size_t)v] != id) {
+              vis[(size_t)v] = id;
+              hd[(size_t)v] = hd[(size_t)u] + 1;
+              ord.push_back(v);
+            }
+          }
+        }
+      }
+      // new levels: only the group's own vertices (BFS order is level-monotone)
+      keep.clear();
+      for (int32_t v : ord)
+        if (ing[(size_t)v] == id) keep.push_back(v);
+      std::vector<int64_t> lw2((size_t)maxL + 1, 0);
+      for (int32_t v : keep) lw2[(size_t)hd[(size_t)v]] += 1;
+      const double eps_s = cfg.eps[(size_t)std::min(st, cfg.n_eps - 1)];
+      std::vector<int32_t> win = eps_aggregate(lw2, w, kg, eps_s);
+      std::vector<int32_t> Tq, wq;
+      const size_t nw = win.size() / 3;
+      if (nw > 0) Tq.push_back(win[0]);
+      for (size_t q = 0; q < nw; ++q) {
+        const int32_t f = win[3 * q], e = win[3 * q + 1], b = win[3 * q + 2];
+        Tq.push_back(split_window(lw2, f, e, kg));
+        Tq.push_back(e);
+        wq.push_back(b);
+        wq.push_back(b);
+      }
+      if (Tq.size() >= 3) alg4_balance(Tq, wq, lw2, kg);
+      std::copy(keep.begin(), keep.end(), S->inv.begin() + p0);  // re-permute the group (locality)
+      std::vector<std::pair<int32_t, int32_t>> kids;  // (rows, workers)
+      for (size_t j = 0; j + 1 < Tq.size(); ++j) {
+        int32_t cnt = 0;
+        for (int32_t l = Tq[j]; l < Tq[j + 1]; ++l) cnt += (int32_t)lw2[(size_t)l];
+        kids.push_back({cnt, wq[j]});
+      }
+      int32_t nonempty = 0;
+      for (auto& kd : kids) nonempty += kd.first > 0;
+      if (nonempty < 2) continue;  // no parallelism found: stays a leaf
+      int32_t a = p0;
+      for (size_t j = 0; j < kids.size(); ++j) {
+        // empty groups still count for the red/blue alternation
+        add_node(id, (int32_t)j, a, a + kids[j].first, st, kids[j].second);
+        a += kids[j].first;
+      }
+    }
+    for (int32_t f = 0; f < n; ++f) S->perm[(size_t)S->inv[(size_t)f]] = f;
+    build_permuted();
+    rp = S->prow_ptr.data();
+    pc = S->pcol.data();
+    // leaves (nodes without children) in position order become the groups
+    std::vector<int32_t> nkids(TP.size(), 0);
+    for (size_t v = 1; v < TP.size(); ++v) nkids[(size_t)TP[v]]++;
+    std::vector<int32_t> leaves;
+    for (size_t v = 1; v < TP.size(); ++v)
+      if (nkids[v] == 0 && T1[v] > T0[v]) leaves.push_back((int32_t)v);
+    std::sort(leaves.begin(), leaves.end(), [&](int32_t a, int32_t b) { return T0[(size_t)a] < T0[(size_t)b]; });
+    S->tree_leaf = leaves;
+    S->level_ptr.assign(1, 0);
+    for (int32_t v : leaves) S->level_ptr.push_back(T1[(size_t)v]);
+    S->group_lvl.resize(leaves.size() + 1);
+    std::iota(S->group_lvl.begin(), S->group_lvl.end(), 0);
+    S->group_workers.assign(leaves.size(), 1);
+    // §5 nrowsEff / eta of the tree, rows as the workload
+    std::vector<int64_t> eff(TP.size(), 0), emax[2];
+    emax[0].assign(TP.size(), 0);
+    emax[1].assign(TP.size(), 0);
+    for (size_t v = TP.size(); v-- > 1;) {  // children have larger ids than parents
+      eff[v] = nkids[v] == 0 ? (int64_t)(T1[v] - T0[v]) : emax[0][v] + emax[1][v];
+      auto& m = emax[(size_t)(TC[v] & 1)][(size_t)TP[v]];
+      m = std::max(m, eff[v]);
+    }
+    eff[0] = emax[0][0] + emax[1][0];
+    S->tree_eta = eff[0] > 0 ? (double)n / ((double)eff[0] * (double)TW[0]) : 1.0;
   }
   const int32_t ngroups = (int32_t)S->group_workers.size();
 
@@ -1077,6 +1210,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     int64_t eff = red + blue;
     S->eta = (eff > 0 && ntiles > 0) ? (double)total_work / ((double)eff * (double)ntiles) : 1.0;
   }
+  if (cfg.scheme == 3) S->eta = S->tree_eta;  // the recursive tree's own §5 eta
   S->build_seconds = now_s() - t0;
   return SYMM_OK;
 }

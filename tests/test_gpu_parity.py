@@ -226,3 +226,28 @@ def test_rcm_schedule(name, variant):
     y_ref = oracle.symmspmv(U, x)
     outs, _, _ = run_gpu(U, x, variant, sched_kw=dict(reorder=2))
     assert relinf(outs[0], y_ref) <= TOL
+
+
+@pytest.mark.parametrize("name,nw", [("st27_24", 296), ("fem_knn_30k", 296), ("spin_14", 592), ("lap2d_64", 64),
+                                     ("lap3d_40", 1184)])
+def test_tree_variant(name, nw):
+    """NEXT-2: the recursive RACE tree (scheme 3) in one persistent launch with
+    tree-scoped counters (K7): matches the oracle, bitwise deterministic; the
+    other variants run the same schedule."""
+    U, x = gen.make_config(name)
+    y_ref = oracle.symmspmv(U, x)
+    outs, plan, s = run_gpu(U, x, "tree", sched_kw=dict(scheme=3, n_workers=nw), repeats=3)
+    assert relinf(outs[0], y_ref) <= TOL
+    assert all(np.array_equal(o, outs[0]) for o in outs[1:])
+    for v in ("colored", "tiled_atomic", "tiled"):
+        (y,), _, _ = run_gpu(U, x, v, sched_kw=dict(scheme=3, n_workers=nw))
+        assert relinf(y, y_ref) <= TOL, v
+
+
+def test_tree_variant_needs_tree_schedule():
+    _torch()
+    import paper_1907_06487_b200 as P
+
+    U = gen.lap2d(16)
+    with pytest.raises(P.SymmError):
+        P.Plan(P.build_schedule(U), U, variant="tree")
