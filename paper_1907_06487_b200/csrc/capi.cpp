@@ -259,6 +259,11 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
   double gain = 0.25;
   if (const char* v = std::getenv("SYMM_SORT_GAIN")) gain = std::atof(v);
   std::vector<char> sort_tile((size_t)nt, 0);
+  std::vector<int64_t> lane_off((size_t)nt + 1, 0);
+  for (int32_t t = 0; t < nt; ++t)
+    lane_off[(size_t)t + 1] = lane_off[(size_t)t] + (S.tile_ptr[(size_t)t + 1] - S.tile_ptr[(size_t)t]) +
+                              (slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
+  std::vector<int32_t> lane_slot((size_t)lane_off[(size_t)nt]), vstart((size_t)n, 0), tile_pads((size_t)nt, 0);
 #pragma omp parallel for schedule(dynamic, 64)
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
@@ -280,21 +285,90 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     std::vector<int32_t> ws(work);
     std::sort(ws.begin(), ws.end(), std::greater<int32_t>());
     sort_tile[(size_t)t] = W > 32 && (double)steps(ws) <= (1.0 - gain) * (double)steps(work);
+    // lane position -> window slot
+    int32_t* sa = lane_slot.data() + lane_off[(size_t)t];
+    for (int32_t i = 0; i < W; ++i) sa[i] = i;
+    if (sort_tile[(size_t)t])
+      std::stable_sort(sa, sa + W, [&](int32_t a, int32_t b) { return work[(size_t)a] > work[(size_t)b]; });
+    // row segments of the 32 lanes of a warp placed so that within each half
+    // warp the segment starts are distinct mod 16: the lanes' lock-step val
+    // loads then hit distinct bank pairs (pad entries where no row fits)
+    int32_t cur = 0, pads = 0;
+    for (int32_t g0 = 0; g0 < W; g0 += 32) {
+      std::vector<int32_t> rem;  // lanes of this warp with a row segment
+      for (int32_t i = g0; i < std::min(W, g0 + 32); ++i)
+        if (sa[i] < T) rem.push_back(i);
+      uint32_t used[2] = {0, 0};
+      int nrem[2] = {0, 0};
+      for (int32_t i : rem) nrem[(i - g0) >> 4]++;
+      while (!rem.empty()) {
+        const int32_t r = cur & 15;
+        int best = -1, bsc = -1;
+        for (size_t q = 0; q < rem.size(); ++q) {
+          const int h = (rem[q] - g0) >> 4;
+          if ((used[h] >> r) & 1) continue;
+          const int32_t len = S.prow_ptr[(size_t)(r0 + sa[rem[q]]) + 1] - S.prow_ptr[(size_t)(r0 + sa[rem[q]])];
+          const int32_t er = (cur + len) & 15;
+          int sc = 0;  // halves that can still use the residue this row ends on
+          for (int h2 = 0; h2 < 2; ++h2)
+            if (nrem[h2] - (h2 == h) > 0 && !((used[h2] | (h2 == h ? 1u << r : 0u)) >> er & 1)) ++sc;
+          if (sc > bsc) { bsc = sc; best = (int)q; }
+        }
+        if (best < 0) { ++cur; ++pads; continue; }  // no row can start here: pad entry
+        const int32_t i = rem[(size_t)best];
+        const int h = (i - g0) >> 4;
+        const int32_t row = r0 + sa[i];
+        vstart[(size_t)row] = cur;
+        cur += S.prow_ptr[(size_t)row + 1] - S.prow_ptr[(size_t)row];
+        used[h] |= 1u << r;
+        nrem[h]--;
+        rem.erase(rem.begin() + best);
+      }
+    }
+    tile_pads[(size_t)t] = pads;
+  }
+  // the ring depth follows the largest block: pad entries must not grow it.
+  // A tile whose padded block would exceed the largest unpadded block keeps
+  // its segments contiguous (no pads; bank-pair starts not guaranteed).
+  auto block_size = [&](int32_t t, int64_t pads) -> int64_t {
+    const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
+    const int64_t S_ = slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t], W = T + S_;
+    const int64_t nnz0 = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
+    int64_t nd = 0;
+    for (int32_t r = r0; r < r1; ++r) nd += (S.prow_ptr[(size_t)r + 1] > S.prow_ptr[(size_t)r] && S.pcol[(size_t)S.prow_ptr[(size_t)r]] == r);
+    int64_t o = align16((int64_t)sizeof(TileDesc) + 4 * (int64_t)T);
+    o = align16(o + 2 * (nnz0 + pads));
+    o = align16(o + 4 * (nnz0 - nd));
+    o = align16(o + 2 * (W + 1));
+    if (sort_tile[(size_t)t]) o = align16(o + 2 * W);
+    o = align16(o + 4 * S_);
+    return align16(o + 8 * (nnz0 + pads));
+  };
+  {
+    int64_t cap0 = 0;
+    for (int32_t t = 0; t < nt; ++t) cap0 = std::max(cap0, block_size(t, 0));
+    for (int32_t t = 0; t < nt; ++t)
+      if (tile_pads[(size_t)t] > 0 && block_size(t, tile_pads[(size_t)t]) > cap0) {
+        const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1];
+        for (int32_t r = r0; r < r1; ++r) vstart[(size_t)r] = S.prow_ptr[(size_t)r] - S.prow_ptr[(size_t)r0];
+        tile_pads[(size_t)t] = 0;
+      }
   }
   int32_t block_cap = 16, window_cap = 2, nnz_cap = 2;
   int bad = 0;
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
     const int32_t S_ = (int32_t)(slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
-    const int64_t nnz = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
+    const int64_t nnz0 = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
+    const int64_t nnz = nnz0 + tile_pads[(size_t)t];  // entry slots incl. placement pads
     int32_t nd = 0;
     for (int32_t r = r0; r < r1; ++r)
       for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
     const int64_t W = (int64_t)T + S_;
     const int64_t o_start = (int64_t)sizeof(TileDesc);
-    int64_t o_lcol = align16(o_start + 2 * (int64_t)(T + 1));
+    int64_t o_lcol = align16(o_start + 4 * (int64_t)T);  // rseg u32[T]: start | length << 16
     int64_t o_tidx = align16(o_lcol + 2 * nnz);
-    int64_t o_tptr = align16(o_tidx + 4 * (nnz - nd));
+    int64_t o_tptr = align16(o_tidx + 4 * (nnz0 - nd));
     // lane positions sorted by work when that shortens the warps' lock-step
     // lists enough (decided below, per tile)
     const int srt = sort_tile[(size_t)t];
@@ -351,7 +425,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     const int32_t r0 = D.row0, T = D.nrows, r1 = r0 + T, ns = D.nspill, W = T + ns;
     unsigned char* blk = blocks.data() + D.block_off;
     std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
-    uint16_t* start = reinterpret_cast<uint16_t*>(blk + sizeof(TileDesc));
+    uint32_t* rseg = reinterpret_cast<uint32_t*>(blk + sizeof(TileDesc));
     uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
     uint32_t* tcsc = reinterpret_cast<uint32_t*>(blk + D.o_tidx);
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
@@ -363,6 +437,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     const SpillRun* tr = runs.data() + run_ptr[(size_t)t];
     const int32_t nrt = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
     const bool bank_aware = !std::getenv("SYMM_NO_BANK_ORDER");
+    const int csc_passes = std::getenv("SYMM_CSC_PASSES") ? std::max(1, std::atoi(std::getenv("SYMM_CSC_PASSES"))) : 8;
     // window id of every entry's column; list lengths of every slot
     const int32_t nnz = D.nnz;
     std::vector<int32_t> eloc((size_t)nnz);
@@ -376,13 +451,15 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         if (S.pcol[(size_t)i] != r) cl[(size_t)lc]++;
       }
     }
-    // lane position -> window slot
-    std::vector<int32_t> slot_at((size_t)W);
-    for (int32_t i = 0; i < W; ++i) slot_at[(size_t)i] = i;
+    // lane position -> window slot (decided with the segment placement)
+    std::vector<int32_t> slot_at(lane_slot.begin() + lane_off[(size_t)t], lane_slot.begin() + lane_off[(size_t)t + 1]);
+    // own row l's segment: entries [rst[l], rst[l] + rl[l]) of lcol / val
+    std::vector<int32_t> rst((size_t)std::max(T, 1), 0);
+    for (int32_t l = 0; l < T; ++l) {
+      rst[(size_t)l] = vstart[(size_t)(r0 + l)];
+      rseg[l] = (uint32_t)rst[(size_t)l] | ((uint32_t)rl[(size_t)l] << 16);
+    }
     if (D.sorted) {
-      std::stable_sort(slot_at.begin(), slot_at.end(), [&](int32_t a, int32_t b) {
-        return rl[(size_t)a] + cl[(size_t)a] > rl[(size_t)b] + cl[(size_t)b];
-      });
       uint16_t* sid = reinterpret_cast<uint16_t*>(blk + D.o_sid);
       for (int32_t i = 0; i < W; ++i) sid[i] = (uint16_t)slot_at[(size_t)i];
     }
@@ -404,28 +481,26 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         const int32_t l = slot_at[(size_t)i];
         if (l >= T) continue;
         const auto& e = ent[(size_t)(i - g0)];
-        const int32_t b = S.prow_ptr[(size_t)(r0 + l)] - e0;
-        start[l] = (uint16_t)b;
+        const int32_t b = rst[(size_t)l];
         for (size_t k = 0; k < e.size(); ++k) {
           lcol[b + (int32_t)k] = e[k].first;
           val[b + (int32_t)k] = e[k].second;
         }
       }
     }
-    start[T] = (uint16_t)(S.prow_ptr[(size_t)r1] - e0);
     // transposed part: slot l's list of (entry, local row), walked after the
     // row part in the same lock step; at each step the lanes of a half warp
     // should read val[entry] and xs[row] from bank pairs not used by the
     // other lanes (including those still in their row part)
     std::vector<std::vector<uint32_t>> lists((size_t)W);
     for (int32_t l = 0; l < T; ++l)
-      for (int32_t k = start[l]; k < start[l + 1]; ++k)
+      for (int32_t k = rst[(size_t)l]; k < rst[(size_t)l] + rl[(size_t)l]; ++k)
         if (lcol[k] != l) lists[lcol[k]].push_back((uint32_t)k | ((uint32_t)l << 16));
     const int32_t vb = (int32_t)(D.o_val / 8);  // bank-pair phase of val[0]
     // sorted tiles walk one list per lane (row part, then transposed part) in
     // lock step; unsorted tiles walk the two parts as separate lock-step loops
     const bool uni = D.sorted != 0;
-    auto rlen = [&](int32_t l) { return (uni && l < T) ? (int32_t)(start[l + 1] - start[l]) : 0; };
+    auto rlen = [&](int32_t l) { return (uni && l < T) ? rl[(size_t)l] : 0; };
     if (bank_aware)
       for (int32_t g0 = 0; g0 < W; g0 += 32) {
         const int32_t g1 = std::min(W, g0 + 32);
@@ -437,30 +512,62 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         for (int32_t j = 0; j < maxlen; ++j)
           for (int32_t h = g0; h < g1; h += 16) {
             const int32_t h1 = std::min(g1, h + 16);
-            uint32_t usedv = 0, usedr = 0;
+            // bank-pair load counts of this (step, half warp): lanes still in
+            // their row part are fixed; each lane in its transposed part picks
+            // one of its remaining entries.  Several greedy passes (lane orders)
+            // minimise max val load + max x load (= wavefronts of the 2 loads).
+            int cv0[16] = {0}, cr0[16] = {0};
+            int act[16], na = 0;
             for (int32_t i = h; i < h1; ++i) {
               const int32_t l = slot_at[(size_t)i];
               if (j < rlen(l)) {
-                const int32_t k = start[l] + j;
-                usedv |= 1u << ((k + vb) & 15);
-                usedr |= 1u << (lcol[k] & 15);
+                const int32_t k = rst[(size_t)l] + j;
+                cv0[(k + vb) & 15]++;
+                cr0[lcol[k] & 15]++;
+              }
+              const int32_t jj = j - rlen(l);
+              if (jj >= 0 && jj < (int32_t)lists[(size_t)l].size()) act[na++] = i;
+            }
+            if (na == 0) continue;
+            int best_cost = INT32_MAX;
+            size_t best_pick[16], pick[16];
+            uint32_t rs = 0x9e3779b9u ^ (uint32_t)(j * 131 + h);
+            for (int pass = 0; pass < csc_passes; ++pass) {
+              int ord[16];
+              for (int q = 0; q < na; ++q) ord[q] = q;
+              if (pass > 0)
+                for (int q = na - 1; q > 0; --q) {  // deterministic shuffle
+                  rs = rs * 1664525u + 1013904223u;
+                  std::swap(ord[q], ord[(int)((rs >> 8) % (uint32_t)(q + 1))]);
+                }
+              int cv[16], cr[16];
+              std::copy(cv0, cv0 + 16, cv);
+              std::copy(cr0, cr0 + 16, cr);
+              for (int q = 0; q < na; ++q) {
+                const int32_t l = slot_at[(size_t)act[ord[q]]];
+                const auto& L = lists[(size_t)l];
+                const size_t jj = (size_t)(j - rlen(l));
+                size_t bq = jj;
+                int bsc = INT32_MAX;
+                for (size_t e = jj; e < L.size(); ++e) {
+                  const int sc = 4 * (cv[((L[e] & 0xffffu) + vb) & 15] + cr[(L[e] >> 16) & 15]) +
+                                 (cv[((L[e] & 0xffffu) + vb) & 15] > 0) + (cr[(L[e] >> 16) & 15] > 0);
+                  if (sc < bsc) { bsc = sc; bq = e; if (sc == 0) break; }
+                }
+                pick[ord[q]] = bq;
+                cv[((L[bq] & 0xffffu) + vb) & 15]++;
+                cr[(L[bq] >> 16) & 15]++;
+              }
+              const int cost = *std::max_element(cv, cv + 16) + *std::max_element(cr, cr + 16);
+              if (cost < best_cost) {
+                best_cost = cost;
+                std::copy(pick, pick + na, best_pick);
               }
             }
-            for (int32_t i = h; i < h1; ++i) {
-              const int32_t l = slot_at[(size_t)i];
+            for (int q = 0; q < na; ++q) {
+              const int32_t l = slot_at[(size_t)act[q]];
               auto& L = lists[(size_t)l];
-              const int32_t jj = j - rlen(l);
-              if (jj < 0 || jj >= (int32_t)L.size()) continue;
-              size_t best = (size_t)jj;
-              int bestscore = -1;
-              for (size_t q = (size_t)jj; q < L.size(); ++q) {
-                const uint32_t bv = (uint32_t)(((L[q] & 0xffffu) + vb) & 15), br = (L[q] >> 16) & 15;
-                const int sc = (((usedv >> bv) & 1) ? 0 : 2) + (((usedr >> br) & 1) ? 0 : 1);
-                if (sc > bestscore) { bestscore = sc; best = q; if (sc == 3) break; }
-              }
-              std::swap(L[(size_t)jj], L[best]);
-              usedv |= 1u << (((L[(size_t)jj] & 0xffffu) + vb) & 15);
-              usedr |= 1u << ((L[(size_t)jj] >> 16) & 15);
+              std::swap(L[(size_t)(j - rlen(l))], L[best_pick[q]]);
             }
           }
       }

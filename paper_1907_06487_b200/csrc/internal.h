@@ -77,10 +77,13 @@ constexpr uint32_t kIdxMask = 0x7fffffffu;
 
 // One tile of the streaming tiled kernels (K3 deterministic / K4 atomic).
 // The tile's block (one cp.async.bulk into shared memory) holds, 16-B aligned:
-//   TileDesc (64 B) | start u16[T+1] | lcol u16[nnz] | tcsc u32[noff] |
+//   TileDesc (64 B) | rseg u32[T] | lcol u16[nnz] | tcsc u32[noff] |
 //   tptr u16[W+1] | [sid u16[W]] | tgt i32[S] | val f64[nnz]
-// start: entry offsets of the T own rows (natural row order); lcol: local
-// column of each entry (own rows 0..T-1, then spill targets T..W-1);
+// rseg: own row l's entries are [start, start + len) of lcol / val, packed
+// start | len << 16; the segments of a warp's rows are placed (with unused pad
+// entries counted in nnz) so that the rows of each half warp start on distinct
+// bank pairs; lcol: local column of each entry (own rows 0..T-1, then spill
+// targets T..W-1);
 // tcsc/tptr: the off-diagonal entries grouped by local target (CSC of the
 // tile), each as (entry index | local row << 16), one list per lane
 // position i (tptr[i] .. tptr[i+1]); sid (sorted tiles only): the window

@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const TileDesc& D = *reinterpret_cast<const TileDesc*>(blk);
     const int T = D.nrows, S = D.nspill, W = T + S, row0 = D.row0;
     const double* xs = reinterpret_cast<const double*>(blk + A.block_cap) + (((uintptr_t)(x + row0) >> 3) & 1);
-    const uint16_t* start = reinterpret_cast<const uint16_t*>(blk + sizeof(TileDesc));
+    const uint32_t* rseg = reinterpret_cast<const uint32_t*>(blk + sizeof(TileDesc));  // start | len << 16
     const uint16_t* lcol = reinterpret_cast<const uint16_t*>(blk + D.o_lcol);
     const uint32_t* tcsc = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
@@ -559,7 +559,8 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
         double acc = 0.0;
         if (l < T && !(A.debug_skip & 1)) {
-          const int eb = start[l], ee = start[l + 1];
+          const uint32_t sg = rseg[l];
+          const int eb = (int)(sg & 0xffffu), ee = eb + (int)(sg >> 16);
 #pragma unroll 4
           for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
         }
@@ -580,8 +581,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
         int eb = 0, nr = 0;
         if (l < T && !(A.debug_skip & 1)) {
-          eb = start[l];
-          nr = start[l + 1] - eb;
+          const uint32_t sg = rseg[l];
+          eb = (int)(sg & 0xffffu);
+          nr = (int)(sg >> 16);
         }
         const int jb = tptr[i];
         const int nt = nr + ((A.debug_skip & 2) ? 0 : tptr[i + 1] - jb);

@@ -3,7 +3,7 @@
 The plan's tile blocks (paper_1907_06487_b200/csrc/capi.cpp, build_tiled_host)
 are decoded here in numpy the way k_tiled walks them -- tile descriptor, lane
 positions (work-sorted through sid[] or in slot order), each lane's row part
-(start/lcol/val) then transposed part (tptr/tcsc), the x window of own rows and
+(rseg/lcol/val) then transposed part (tptr/tcsc), the x window of own rows and
 spill targets, the flush targets -- and the decoded SymmSpMV is compared with
 the oracle (Alg. 2).  Independently of the decode, every
 stored off-diagonal entry must be read exactly once by its row's lane and once
@@ -56,7 +56,12 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
         assert hd.tobytes() == D.tobytes()  # the descriptor travels with its block
         T, S, row0, nnz = int(D["nrows"]), int(D["nspill"]), int(D["row0"]), int(D["nnz"])
         W = T + S
-        start = np.frombuffer(b, dtype="<u2", count=T + 1, offset=h + 64).astype(np.int64)
+        rseg = np.frombuffer(b, dtype="<u4", count=T, offset=h + 64).astype(np.int64)
+        rst, rln = rseg & 0xFFFF, rseg >> 16  # own row segments: [rst, rst + rln)
+        seg = np.zeros(nnz, dtype=np.int64)  # segments are disjoint (pads belong to none)
+        for l in range(T):
+            seg[rst[l]:rst[l] + rln[l]] += 1
+        assert seg.max(initial=0) <= 1 and int(seg.sum()) == int(rln.sum())
         lcol = np.frombuffer(b, dtype="<u2", count=nnz, offset=h + int(D["o_lcol"])).astype(np.int64)
         tptr = np.frombuffer(b, dtype="<u2", count=W + 1, offset=h + int(D["o_tptr"])).astype(np.int64)
         noff = int(tptr[W])
@@ -80,17 +85,22 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
             assert np.array_equal(gid[w:w + ln], g + np.arange(ln))
             if int(D["gather_runs"]):
                 assert (w - (g - row0)) % 2 == 0
+        if nnz > int(rln.sum()):  # padded placement: rows of a half warp start on distinct bank pairs
+            for g0 in range(0, W, 16):
+                ls = [int(sid[i]) for i in range(g0, min(W, g0 + 16)) if sid[i] < T]
+                res = [(int(D["o_val"]) // 8 + int(rst[l])) % 16 for l in ls]
+                assert len(set(res)) == len(res)
         for i in range(W):
             l = int(sid[i])
             acc = 0.0
             if l < T:
-                for k in range(int(start[l]), int(start[l + 1])):
+                for k in range(int(rst[l]), int(rst[l] + rln[l])):
                     acc += val[k] * xs[lcol[k]]              # tmp += A[idx] x[col[idx]]
                     row_pairs.append((row0 + l, int(gid[lcol[k]])))
             for j in range(int(tptr[i]), int(tptr[i + 1])):
                 q = int(tcsc[j])
                 e, r = q & 0xFFFF, q >> 16
-                assert r < T and lcol[e] == l and start[r] <= e < start[r + 1]
+                assert r < T and lcol[e] == l and rst[r] <= e < rst[r] + rln[r]
                 acc += val[e] * xs[r]                          # b[col] += A[idx] x[row]
                 csc_pairs.append((row0 + r, int(gid[l])))
             if gid[l] >= 0:
