@@ -11,6 +11,7 @@
 //     intra-tile distance-2 row coloring, first-writer flags, validator
 //                                                   PAPER.md:1191-1217, 1650-1660, 787-789
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -343,6 +344,11 @@ int32_t pseudo_peripheral(int32_t start, const std::vector<int64_t>& gp, const s
 }
 
 }  // namespace
+
+// K3/K4 ring: kRingStages stages of (tile block + x window) should fit the
+// dynamic shared memory a B200 CTA gets (227 KB - 1 KB reserved - static)
+constexpr int64_t kRingBytes = 232448 - 1024 - 512;
+constexpr int64_t kRingStages = 6;
 
 int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S) {
   const double t0 = now_s();
@@ -723,6 +729,8 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     S->tree_eta = eff[0] > 0 ? (double)n / ((double)eff[0] * (double)TW[0]) : 1.0;
   }
   const int32_t ngroups = (int32_t)S->group_workers.size();
+  int64_t block_budget = 0;  // 0: derived from the ring (below)
+  if (const char* v = std::getenv("SYMM_BLOCK_BUDGET")) block_budget = std::atoll(v);  // diagnostics / sweeps
 
   // ---- a7 tiles --------------------------------------------------------------
   // (a) cone tiles (cfg.cone_tiles, reading R26): inside level group g with b_g
@@ -890,6 +898,27 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   };
   {
     std::vector<std::vector<std::pair<int32_t, int32_t>>> per_group((size_t)ngroups);
+    // K3/K4 tile block (capi.cpp build_tiled_host) bytes, upper bound:
+    // descriptor + rseg 4 B/row + lcol 2 + val 8 + tcsc 4 B per entry +
+    // tptr / sid 2+2 B and tgt 4 B per window slot
+    auto est_block = [&](int32_t nr, int64_t tnnz, int64_t tw) { return 64 + 4 * (int64_t)nr + 14 * tnnz + 8 * tw + 96; };
+    // split [a, b) in halves until every piece meets the row / nnz / window
+    // caps and the block-byte budget
+    auto split_fit = [&](int32_t a0, int32_t b0, int64_t budget, std::vector<std::pair<int32_t, int32_t>>& out) {
+      std::vector<std::pair<int32_t, int32_t>> st{{a0, b0}};
+      while (!st.empty()) {
+        auto rg = st.back();
+        st.pop_back();
+        const int32_t nr = rg.second - rg.first;
+        const int64_t tnnz = rp[rg.second] - rp[rg.first];
+        const int64_t tw = nr <= cfg.max_tile_rows && tnnz <= cfg.max_tile_nnz ? window_of(rg.first, rg.second) : INT64_MAX;
+        const bool fits = tw <= cfg.max_tile_window && est_block(nr, tnnz, tw) <= budget;
+        if (fits || nr == 1) { out.push_back(rg); continue; }
+        const int32_t mid = rg.first + nr / 2;
+        st.push_back({mid, rg.second});
+        st.push_back({rg.first, mid});
+      }
+    };
 #pragma omp parallel for schedule(dynamic, 1)
     for (int32_t g = 0; g < ngroups; ++g) {
       int32_t r0 = S->level_ptr[(size_t)S->group_lvl[(size_t)g]];
@@ -919,23 +948,27 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
       cuts.push_back(r1);
       // caps (stack of ranges, split in half until they fit)
       std::vector<std::pair<int32_t, int32_t>> out;
-      for (size_t c = 0; c + 1 < cuts.size(); ++c) {
-        std::vector<std::pair<int32_t, int32_t>> st{{cuts[c], cuts[c + 1]}};
-        std::vector<std::pair<int32_t, int32_t>> done;
-        while (!st.empty()) {
-          auto rg = st.back();
-          st.pop_back();
-          int32_t nr = rg.second - rg.first;
-          bool fits = nr <= cfg.max_tile_rows && (rp[rg.second] - rp[rg.first]) <= cfg.max_tile_nnz &&
-                      window_of(rg.first, rg.second) <= cfg.max_tile_window;
-          if (fits || nr == 1) { done.push_back(rg); continue; }
-          int32_t mid = rg.first + nr / 2;
-          st.push_back({mid, rg.second});
-          st.push_back({rg.first, mid});
-        }
-        for (auto& d : done) out.push_back(d);
-      }
+      for (size_t c = 0; c + 1 < cuts.size(); ++c) split_fit(cuts[c], cuts[c + 1], INT64_MAX, out);
       per_group[(size_t)g] = out;
+    }
+    // block-byte budget: the kernel's ring holds `stages` x (block + x window);
+    // aim at kRingStages stages with the largest window found, and split the
+    // (few) tiles whose block would force a shallower ring
+    {
+      int64_t maxw = 0;
+      std::vector<std::vector<int64_t>> tws((size_t)ngroups);
+#pragma omp parallel for schedule(dynamic, 1) reduction(max : maxw)
+      for (int32_t g = 0; g < ngroups; ++g)
+        for (auto& rg : per_group[(size_t)g]) maxw = std::max<int64_t>(maxw, window_of(rg.first, rg.second));
+      int64_t budget = kRingBytes / kRingStages - 8 * (((maxw + 2 + 15) / 16) * 16) - 128;
+      if (block_budget > 0) budget = block_budget;  // SYMM_BLOCK_BUDGET (sweeps)
+      budget = std::max<int64_t>(budget, 4096);
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int32_t g = 0; g < ngroups; ++g) {
+        std::vector<std::pair<int32_t, int32_t>> out;
+        for (auto& rg : per_group[(size_t)g]) split_fit(rg.first, rg.second, budget, out);
+        per_group[(size_t)g].swap(out);
+      }
     }
     S->tile_ptr.clear();
     S->tile_group.clear();
