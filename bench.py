@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", default="st27_128")
     ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "tree", "auto"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sweep", default=None, choices=["gs", "kacz"],
+                    help="NEXT-4: time symmetric Gauss-Seidel / Kaczmarz sweeps instead of SymmSpMV (own JSON line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-variants", action="store_true", help="also time the other variants (extra key)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -318,6 +320,60 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
     return 0
 
 
+def run_sweep(a, U, x, s, nf, t_sched):
+    """NEXT-4: symmetric GS / Kaczmarz sweeps (forward + backward), phase by
+    phase on the schedule's level groups; device-timed; one JSON line."""
+    import torch
+
+    import oracle  # parity of the timed configuration on a sample is the oracle's job (tests); here: one check
+    import paper_1907_06487_b200 as P
+
+    n = U.n
+    perm, inv = s.permutation()
+    t0 = time.perf_counter()
+    sw = P.Sweep(s, a.sweep)
+    t_plan = time.perf_counter() - t0
+    rows, ptr = sw.order()
+    rng = np.random.default_rng(7)
+    b = rng.uniform(-1, 1, n)
+    bd = torch.from_numpy(b[inv].copy()).cuda()
+    x0 = torch.from_numpy(x[inv].copy()).cuda()
+    xd = x0.clone()
+    for _ in range(max(3, a.warmup)):
+        sw.run(xd, bd, symmetric=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    xd.copy_(x0)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(a.steps):
+        sw.run(xd, bd, symmetric=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    # one symmetric sweep from x0 against the serial oracle in the plan's order
+    xd.copy_(x0)
+    sw.run(xd, bd, symmetric=True)
+    torch.cuda.synchronize()
+    x_ref = oracle.sweep(a.sweep, U, b, x, inv[rows].astype(np.int32), symmetric=True)
+    err = float(np.max(np.abs(xd.cpu().numpy()[perm] - x_ref)) / max(np.max(np.abs(x_ref)), 1e-300))
+    # algorithmic bytes of a symmetric sweep: 2 x (full matrix 12 B/nnz + row
+    # order / pointers 8 B/row + b 8 B/row + x read + write 16 B/row)
+    byts = 2 * (12 * nf + 32 * n)
+    peak, peak_src = peaks()
+    achieved = byts / (ms * 1e-3) / 1e9
+    line = {"metric": f"symmetric {a.sweep.upper()} sweep (NEXT-4)", "value": 1e3 / ms, "unit": "sweeps/s",
+            "ms_per_step": ms, "steps": a.steps, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": a.config, "n": n, "nnz_full": nf, "phases_per_sweep": int(len(ptr) - 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "bytes_per_launch": byts, "peak_source": peak_src,
+                         "bytes_model": "2 x (12 nnz_full + 32 n): matrix, pointers + order, b, x read + write"},
+            "parity_relinf_vs_serial_oracle": err, "gpu_launches": 2 * int(len(ptr) - 1) * a.steps,
+            "schedule": {"build_s": t_sched, "plan_s": t_plan}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -357,6 +413,8 @@ def main():
         sched_kw[k_] = int(v_)
     s = P.build_schedule(U, **sched_kw)
     t_sched = time.perf_counter() - t0
+    if a.sweep:
+        return run_sweep(a, U, x, s, nf, t_sched)
     st = s.stats
     perm, inv = s.permutation()
     if ws > 1 or a.force_dist:

@@ -240,6 +240,36 @@ int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n);
 
 int symmspmv_destroy(symmspmv_plan_t* p);
 
+/* ---- NEXT-4: distance-k iterative sweeps on the same schedule --------------
+ * SURVEY §8f NEXT-4; the kernels appear in PAPER.md's draft text only
+ * (Gauss-Seidel, distance-1; Kaczmarz, distance-2, "For its
+ * parallelization one typically uses a distance-2 coloring").  The schedule's
+ * level groups already separate same-colour groups by distance >= 3
+ * (PAPER.md:1227-1229); inside every level group the plan colours the rows
+ * greedily, in row order, so that rows of one colour are distance-1 (GS) or
+ * distance-2 (KACZ) independent in the FULL graph of A.  A sweep runs phase by
+ * phase: the red groups' colour 0, 1, ..., then the blue groups' colours; a
+ * backward sweep runs the phases in reverse.  Rows of one phase commute, so
+ * the result equals a serial sweep in the plan's row order
+ * (symm_sweep_order), bit for bit up to the summation order inside a row.
+ *   GS   (kind 1): x_r := (b_r - sum_{c != r} a_rc x_c) / a_rr (textbook
+ *        Gauss-Seidel; every row needs a nonzero stored diagonal, else
+ *        SYMM_ERR_ARG at plan time);
+ *   KACZ (kind 2): x := x + (b_r - <A_r, x>) / ||A_r||^2 * A_r (PAPER.md:
+ *        826-851, eq:KACZ); rows with ||A_r|| = 0 are skipped.
+ * x_dev, b_dev: DEVICE fp64[n] in the schedule's PERMUTED order; x is read and
+ * overwritten; symmetric != 0 appends the backward sweep (SymmGS / SymmKACZ).
+ * The plan owns its device memory (full matrix of the permuted order, row
+ * order, phase table). */
+typedef enum { SYMM_SWEEP_GS = 1, SYMM_SWEEP_KACZ = 2 } symm_sweep_kind;
+typedef struct symm_sweep symm_sweep_t;
+int symm_sweep_plan(const race_schedule_t* s, int32_t kind, int32_t device, symm_sweep_t** out);
+int symm_sweep_run(symm_sweep_t* p, double* x_dev, const double* b_dev, int32_t symmetric, void* stream);
+/* Host copy of the execution order: rows[n] (permuted ids, phase by phase) and
+ * phase_ptr[nphases+1]; *nphases is set; either array may be NULL. */
+int symm_sweep_order(const symm_sweep_t* p, int32_t* rows, int32_t* phase_ptr, int32_t* nphases);
+int symm_sweep_destroy(symm_sweep_t* p);
+
 const char* symm_status_string(int status);
 const char* symm_last_error(void);
 

@@ -40,6 +40,10 @@ def _lib():
         L.oracle_symmspmv_ld.restype = None
         L.oracle_symmspmv_omp.argtypes = [i32, vp, vp, vp, vp, vp, i32]
         L.oracle_symmspmv_omp.restype = i32
+        L.oracle_gs_sweep.argtypes = [i32, vp, vp, vp, vp, vp, vp, i64]
+        L.oracle_gs_sweep.restype = None
+        L.oracle_kacz_sweep.argtypes = [i32, vp, vp, vp, vp, vp, vp, i64]
+        L.oracle_kacz_sweep.restype = None
         L.oracle_mirror.argtypes = [i32, vp, vp, vp, vp, vp, vp]
         L.oracle_mirror.restype = i64
         L.oracle_spmv.argtypes = [i32, vp, vp, vp, vp, vp]
@@ -116,6 +120,20 @@ def spmv(rp, col, val, x) -> np.ndarray:
     y = np.empty(n, dtype=np.float64)
     _lib().oracle_spmv(n, _p(rp), _p(col), _p(val), _p(x), _p(y))
     return y
+
+
+def sweep(kind: str, U, b, x0, order, symmetric: bool = False) -> np.ndarray:
+    """One serial Gauss-Seidel ("gs") or Kaczmarz ("kacz") sweep over the rows
+    in `order` (then in reverse if symmetric) on the full matrix of U
+    (readings R32-R33); returns the new x."""
+    rp, col, val = mirror(U)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.array(x0, dtype=np.float64, copy=True)
+    f = _lib().oracle_gs_sweep if kind == "gs" else _lib().oracle_kacz_sweep
+    for o in ([order, order[::-1]] if symmetric else [order]):
+        o = np.ascontiguousarray(o, dtype=np.int32)
+        f(U.n, _p(rp), _p(col), _p(val), _p(b), _p(x), _p(o), len(o))
+    return x
 
 
 def dense_matvec(Ad, x) -> np.ndarray:

@@ -190,6 +190,47 @@ void oracle_spmv(int32_t n, const int32_t* rowPtr, const int32_t* col, const dou
   }
 }
 
+/* ---------------------------------------------------------------------------
+ * NEXT-4 distance-k kernels (draft text of the paper), one
+ * serial sweep over the rows in the given order on the FULL matrix (CRS,
+ * e.g. from oracle_mirror).
+ * Gauss-Seidel, textbook form (reading R32: the draft Alg. GS, PAPER.md:
+ * 793-806, adds b to the old x[row]; we use x_r := (b_r - sum_{c != r} a_rc
+ * x_c) / a_rr, the fixed point of which is A x = b):
+ * ------------------------------------------------------------------------- */
+void oracle_gs_sweep(int32_t n, const int32_t* rowPtr, const int32_t* col, const double* A, const double* b,
+                     double* x, const int32_t* order, int64_t m) {
+  (void)n;
+  for (int64_t q = 0; q < m; ++q) {
+    const int32_t row = order[q];
+    double s = 0.0, diag = 0.0;
+    for (int32_t idx = rowPtr[row]; idx < rowPtr[row + 1]; ++idx) {
+      if (col[idx] == row) diag += A[idx];
+      else s += A[idx] * x[col[idx]];
+    }
+    x[row] = (b[row] - s) / diag;
+  }
+}
+
+/* Kaczmarz row projections, Alg. KACZ / eq:KACZ (PAPER.md:
+ * 828-831): scale = (b_r - <A_r, x>) / ||A_r||^2, then x_c += scale * a_rc for
+ * every c in row r; rows with ||A_r|| = 0 are skipped. */
+void oracle_kacz_sweep(int32_t n, const int32_t* rowPtr, const int32_t* col, const double* A, const double* b,
+                       double* x, const int32_t* order, int64_t m) {
+  (void)n;
+  for (int64_t q = 0; q < m; ++q) {
+    const int32_t row = order[q];
+    double scale = b[row], rownorm = 0.0;
+    for (int32_t idx = rowPtr[row]; idx < rowPtr[row + 1]; ++idx) {
+      scale -= A[idx] * x[col[idx]];
+      rownorm += A[idx] * A[idx];
+    }
+    if (rownorm == 0.0) continue;
+    scale = scale / rownorm;
+    for (int32_t idx = rowPtr[row]; idx < rowPtr[row + 1]; ++idx) x[col[idx]] += scale * A[idx];
+  }
+}
+
 /* Dense y = A x for tiny matrices given as a dense row-major array (the
  * textbook definition y_i = sum_j A_ij x_j, "b = Ax"). */
 void oracle_dense_matvec(int32_t n, const double* Ad, const double* x, double* y) {

@@ -16,7 +16,7 @@ import numpy as np
 from . import _lib
 from ._lib import (SYMM_ORDER_ORIGINAL, SYMM_ORDER_PERMUTED, VARIANTS, SymmError, check, lib)
 
-__all__ = ["build_schedule", "Schedule", "Plan", "VARIANTS", "SymmError", "min_bytes", "flops",
+__all__ = ["build_schedule", "Schedule", "Plan", "Sweep", "VARIANTS", "SymmError", "min_bytes", "flops",
            "SYMM_ORDER_PERMUTED", "SYMM_ORDER_ORIGINAL", "library_path"]
 
 library_path = _lib.LIB_PATH
@@ -215,3 +215,37 @@ class Plan:
         d, m = C.c_int64(0), C.c_int64(0)
         check(lib().symmspmv_plan_bytes(self._h, C.byref(d), C.byref(m)))
         return d.value, m.value
+
+
+class Sweep:
+    """symm_sweep_t (NEXT-4): Gauss-Seidel ("gs", distance-1) or Kaczmarz
+    ("kacz", distance-2) sweeps phase by phase on the schedule's level groups,
+    rows coloured inside every group (include/symmspmv.h)."""
+
+    KINDS = {"gs": 1, "kacz": 2}
+
+    def __init__(self, sched: Schedule, kind: str = "kacz", device: int = 0):
+        h = C.c_void_p()
+        check(lib().symm_sweep_plan(sched._h, self.KINDS[kind], device, C.byref(h)))
+        self._h = h
+        self.n = sched.n
+        self.kind = kind
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().symm_sweep_destroy(self._h)
+            self._h = None
+
+    def run(self, x, b, symmetric: bool = True, stream=None):
+        """x := sweep(x) (device tensors in the permuted order, asynchronous)."""
+        check(lib().symm_sweep_run(self._h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(b)), int(symmetric),
+                                   C.c_void_p(_stream(stream))))
+
+    def order(self):
+        """(rows in execution order (permuted ids), phase_ptr)."""
+        npz = C.c_int32(0)
+        check(lib().symm_sweep_order(self._h, None, None, C.byref(npz)))
+        rows = np.zeros(self.n, dtype=np.int32)
+        ptr = np.zeros(npz.value + 1, dtype=np.int32)
+        check(lib().symm_sweep_order(self._h, rows.ctypes.data, ptr.ctypes.data, C.byref(npz)))
+        return rows, ptr

@@ -50,7 +50,7 @@ EXPORTS = [
     "race_schedule_table", "race_schedule_permuted_matrix", "race_schedule_destroy", "race_schedule_partition",
     "symmspmv_options_default", "symmspmv_plan", "symmspmv_plan_rows", "symmspmv_plan_local", "symmspmv_halo_add", "symmspmv_run", "symmspmv_run_variant", "symmspmv_run_host",
     "symmspmv_last_launches", "symmspmv_plan_bytes", "symmspmv_plan_info", "symmspmv_destroy", "symm_status_string",
-    "symm_last_error",
+    "symm_last_error", "symm_sweep_plan", "symm_sweep_run", "symm_sweep_order", "symm_sweep_destroy",
 ]
 
 _LIB = None
@@ -85,6 +85,10 @@ def lib():
             "symmspmv_plan_bytes": ([vp, vp, vp], C.c_int),
             "symmspmv_plan_info": ([vp, vp, i32], C.c_int),
             "symmspmv_destroy": ([vp], C.c_int),
+            "symm_sweep_plan": ([vp, i32, i32, vp], C.c_int),
+            "symm_sweep_run": ([vp, vp, vp, i32, vp], C.c_int),
+            "symm_sweep_order": ([vp, vp, vp, vp], C.c_int),
+            "symm_sweep_destroy": ([vp], C.c_int),
             "symm_status_string": ([C.c_int], C.c_char_p),
             "symm_last_error": ([], C.c_char_p),
         }

@@ -1382,6 +1382,163 @@ extern "C" int symm_tiled_format_dump(const race_schedule_t* s, int64_t* sizes, 
   return SYMM_OK;
 }
 
+// ---- NEXT-4 sweeps (GS distance-1, KACZ distance-2) on the schedule --------
+}  // extern "C"
+
+struct symm_sweep {
+  symmspmv_plan_t* P = nullptr;   // device buffers + device id
+  int kind = 0;
+  int32_t n = 0;
+  int vec = 4;
+  int32_t *d_rp = nullptr, *d_col = nullptr, *d_rows = nullptr;
+  double* d_val = nullptr;
+  std::vector<int32_t> rows, phase_ptr;
+};
+
+extern "C" {
+
+int symm_sweep_plan(const race_schedule_t* s, int32_t kind, int32_t device, symm_sweep_t** out) {
+  clear_error();
+  if (!s || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  if (kind != SYMM_SWEEP_GS && kind != SYMM_SWEEP_KACZ) return set_error(SYMM_ERR_ARG, "sweep kind %d", kind);
+  const Schedule& S = s->S;
+  const int32_t n = S.n;
+  // full matrix A' of the permuted order (CRS, columns ascending, diagonal included)
+  std::vector<int64_t> cnt((size_t)n + 1, 0);
+  for (int32_t r = 0; r < n; ++r)
+    for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+      cnt[(size_t)r + 1]++;
+      if (S.pcol[(size_t)i] != r) cnt[(size_t)S.pcol[(size_t)i] + 1]++;
+    }
+  for (int32_t r = 0; r < n; ++r) cnt[(size_t)r + 1] += cnt[(size_t)r];
+  if (cnt[(size_t)n] >= ((int64_t)1 << 31)) return set_error(SYMM_ERR_OVERFLOW, "full matrix has >= 2^31 entries");
+  std::vector<int32_t> rp((size_t)n + 1), col((size_t)cnt[(size_t)n]);
+  std::vector<double> val((size_t)cnt[(size_t)n]);
+  for (int32_t r = 0; r <= n; ++r) rp[(size_t)r] = (int32_t)cnt[(size_t)r];
+  {
+    std::vector<int32_t> pos(rp.begin(), rp.end() - 1);
+    for (int32_t c = 0; c < n; ++c)
+      for (int32_t i = S.prow_ptr[(size_t)c]; i < S.prow_ptr[(size_t)c + 1]; ++i) {
+        const int32_t r = S.pcol[(size_t)i];
+        if (r == c) continue;
+        col[(size_t)pos[(size_t)r]] = c;
+        val[(size_t)pos[(size_t)r]++] = S.pval[(size_t)i];
+      }
+    for (int32_t r = 0; r < n; ++r)
+      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) {
+        col[(size_t)pos[(size_t)r]] = S.pcol[(size_t)i];
+        val[(size_t)pos[(size_t)r]++] = S.pval[(size_t)i];
+      }
+  }
+  if (kind == SYMM_SWEEP_GS)
+    for (int32_t r = 0; r < n; ++r) {
+      bool diag = false;
+      for (int32_t i = rp[(size_t)r]; i < rp[(size_t)r + 1]; ++i) diag |= (col[(size_t)i] == r && val[(size_t)i] != 0.0);
+      if (!diag) return set_error(SYMM_ERR_ARG, "Gauss-Seidel needs a nonzero diagonal (row %d of the permuted matrix)", r);
+    }
+  // colours inside every level group: greedy in row order; a row conflicts
+  // with the earlier rows of its group at distance 1 (GS) or <= 2 (KACZ)
+  const int32_t ng = (int32_t)S.group_workers.size();
+  std::vector<int32_t> colour((size_t)n, 0), gof((size_t)n, 0), ncol((size_t)std::max(ng, 1), 0);
+  for (int32_t g = 0; g < ng; ++g)
+    for (int32_t r = S.level_ptr[(size_t)S.group_lvl[(size_t)g]]; r < S.level_ptr[(size_t)S.group_lvl[(size_t)g + 1]]; ++r)
+      gof[(size_t)r] = g;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int32_t g = 0; g < ng; ++g) {
+    const int32_t a = S.level_ptr[(size_t)S.group_lvl[(size_t)g]], b = S.level_ptr[(size_t)S.group_lvl[(size_t)g + 1]];
+    std::vector<char> used;
+    for (int32_t r = a; r < b; ++r) {
+      std::fill(used.begin(), used.end(), 0);
+      auto forbid = [&](int32_t q) {
+        if (q >= a && q < r && gof[(size_t)q] == g) {
+          const int32_t c = colour[(size_t)q];
+          if ((size_t)c >= used.size()) used.resize((size_t)c + 1, 0);
+          used[(size_t)c] = 1;
+        }
+      };
+      for (int32_t i = rp[(size_t)r]; i < rp[(size_t)r + 1]; ++i) {
+        const int32_t c = col[(size_t)i];
+        forbid(c);
+        if (kind == SYMM_SWEEP_KACZ)
+          for (int32_t k = rp[(size_t)c]; k < rp[(size_t)c + 1]; ++k) forbid(col[(size_t)k]);
+      }
+      int32_t c = 0;
+      while ((size_t)c < used.size() && used[(size_t)c]) ++c;
+      colour[(size_t)r] = c;
+      ncol[(size_t)g] = std::max(ncol[(size_t)g], c + 1);
+    }
+  }
+  int32_t nc[2] = {0, 0};
+  for (int32_t g = 0; g < ng; ++g) nc[g & 1] = std::max(nc[g & 1], ncol[(size_t)g]);
+  auto phase_of = [&](int32_t r) { const int32_t g = gof[(size_t)r]; return (g & 1) ? nc[0] + colour[(size_t)r] : colour[(size_t)r]; };
+  symm_sweep_t* W = new symm_sweep_t();
+  W->kind = kind;
+  W->n = n;
+  const int32_t np = nc[0] + nc[1];
+  W->phase_ptr.assign((size_t)np + 1, 0);
+  for (int32_t r = 0; r < n; ++r) W->phase_ptr[(size_t)phase_of(r) + 1]++;
+  for (int32_t p = 0; p < np; ++p) W->phase_ptr[(size_t)p + 1] += W->phase_ptr[(size_t)p];
+  W->rows.assign((size_t)n, 0);
+  {
+    std::vector<int32_t> pos(W->phase_ptr.begin(), W->phase_ptr.end() - 1);
+    for (int32_t r = 0; r < n; ++r) W->rows[(size_t)pos[(size_t)phase_of(r)]++] = r;  // ascending rows per phase
+  }
+  {
+    const double avg = n > 0 ? (double)col.size() / n : 1.0;
+    int v = 1;
+    while (v < 32 && 2.0 * v <= avg / 1.5) v *= 2;
+    W->vec = v;
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  W->P = new symmspmv_plan_t();
+  W->P->device = device;
+  int rc;
+  if ((rc = upload(W->P, &W->d_rp, rp.data(), rp.size())) || (rc = upload(W->P, &W->d_col, col.data(), col.size())) ||
+      (rc = upload(W->P, &W->d_val, val.data(), val.size())) || (rc = upload(W->P, &W->d_rows, W->rows.data(), W->rows.size()))) {
+    cudaSetDevice(cur);
+    free_plan(W->P);
+    delete W;
+    return rc;
+  }
+  cudaSetDevice(cur);
+  *out = W;
+  return SYMM_OK;
+}
+
+int symm_sweep_run(symm_sweep_t* W, double* x, const double* b, int32_t symmetric, void* stream) {
+  clear_error();
+  if (!W || (W->n > 0 && (!x || !b))) return set_error(SYMM_ERR_ARG, "NULL argument");
+  if ((const void*)x == (const void*)b) return set_error(SYMM_ERR_ALIAS, "x and b alias");
+  const CsrArgs A{W->n, W->d_rp, W->d_col, W->d_val};
+  const int32_t np = (int32_t)W->phase_ptr.size() - 1;
+  for (int dir = 0; dir < (symmetric ? 2 : 1); ++dir)
+    for (int32_t q = 0; q < np; ++q) {
+      const int32_t p = dir == 0 ? q : np - 1 - q;  // backward sweep: phases in reverse
+      const int32_t a = W->phase_ptr[(size_t)p], e = W->phase_ptr[(size_t)p + 1];
+      int rc = launch_sweep_phase(W->kind, A, W->d_rows + a, e - a, b, x, W->vec, stream);
+      if (rc) return cuda_fail((cudaError_t)rc, "k_sweep");
+    }
+  return SYMM_OK;
+}
+
+int symm_sweep_order(const symm_sweep_t* W, int32_t* rows, int32_t* phase_ptr, int32_t* nphases) {
+  if (!W) return set_error(SYMM_ERR_ARG, "NULL sweep plan");
+  if (nphases) *nphases = (int32_t)W->phase_ptr.size() - 1;
+  if (rows) std::copy(W->rows.begin(), W->rows.end(), rows);
+  if (phase_ptr) std::copy(W->phase_ptr.begin(), W->phase_ptr.end(), phase_ptr);
+  return SYMM_OK;
+}
+
+int symm_sweep_destroy(symm_sweep_t* W) {
+  if (!W) return SYMM_OK;
+  free_plan(W->P);
+  delete W;
+  return SYMM_OK;
+}
+
 int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n) {
   if (!p || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
   int32_t v[8] = {p->variant, p->vec, p->tiled_grid, p->targs.stages, p->targs.block_cap, p->targs.window_cap,

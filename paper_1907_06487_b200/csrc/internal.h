@@ -169,6 +169,10 @@ struct TreeArgs {
 int launch_tree(const CsrArgs& A, const ColoredArgs& C, const TreeArgs& T, const double* x, double* y, int vec,
                 int grid, void* stream);
 
+// ---- NEXT-4 sweeps: one launch per phase, V lanes per row of the full matrix
+int launch_sweep_phase(int kind, const CsrArgs& A, const int32_t* rows, int32_t nrows, const double* b, double* x,
+                       int vec, void* stream);
+
 // ---- K5 colored_smem (cs_build.cpp / kernels.cu) ------------------------------
 // One tile = consecutive schedule tiles of one level group; rows coloured by
 // write sets (RACE distance-2) and executed colour by colour

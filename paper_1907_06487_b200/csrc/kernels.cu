@@ -11,6 +11,7 @@
 //                  passes, staged cross-tile contributions with depth-1
 //                  dependencies -> deterministic, y written once (see below).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.h"
@@ -135,6 +136,49 @@ __global__ void __launch_bounds__(256) k_spmv(CsrArgs A, const double* __restric
     }
     sum = group_sum<V>(sum);
     if (row < A.n && sub == 0) y[row] = sum;
+  }
+}
+
+// ---------------------------------------------------------------- NEXT-4 sweeps
+// One phase of a Gauss-Seidel (KIND 1) or Kaczmarz (KIND 2) sweep: V lanes per
+// row of the full matrix; the rows of a phase are distance-1 (GS) /
+// distance-2 (KACZ) independent, so their reads and writes of x commute.
+template <int KIND, int V>
+__global__ void __launch_bounds__(256) k_sweep(CsrArgs A, const int32_t* __restrict__ rows, int32_t nrows,
+                                               const double* __restrict__ b, double* __restrict__ x) {
+  constexpr int RPW = 32 / V;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % V;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * RPW; base < nrows; base += nwarps * RPW) {  // warp-uniform
+    const int64_t q = base + lane / V;
+    const bool valid = q < nrows;
+    const int row = valid ? rows[q] : 0;
+    const int bi = valid ? A.row_ptr[row] : 0, ei = valid ? A.row_ptr[row + 1] : 0;
+    double s = 0.0, t = 0.0;  // GS: off-diagonal sum, diagonal; KACZ: <A_r, x>, ||A_r||^2
+    for (int i = bi + sub; i < ei; i += V) {
+      const int c = A.col[i];
+      const double a = A.val[i];
+      if (KIND == 1) {
+        if (c == row) t += a;
+        else s += a * __ldcg(x + c);
+      } else {
+        s += a * __ldcg(x + c);
+        t += a * a;
+      }
+    }
+    s = group_sum<V>(s);
+    t = group_sum<V>(t);
+    if (KIND == 1) {
+      if (valid && sub == 0) __stcg(x + row, (b[row] - s) / t);  // x_r := (b_r - sum_{c!=r} a_rc x_c) / a_rr
+    } else if (valid && t > 0.0) {
+      const double scale = (b[row] - s) / t;  // (b_r - <A_r, x>) / ||A_r||^2
+      for (int i = bi + sub; i < ei; i += V) {
+        const int c = A.col[i];
+        __stcg(x + c, __ldcg(x + c) + scale * A.val[i]);  // x_c += scale a_rc (distance-2: no other row of the phase)
+      }
+    }
   }
 }
 
@@ -1003,6 +1047,31 @@ int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x
     case 16: k_colored<16><<<C.nphase_tiles, threads, 0, st>>>(A, C, x, y); break;
     default: k_colored<32><<<C.nphase_tiles, threads, 0, st>>>(A, C, x, y); break;
   }
+  return (int)cudaGetLastError();
+}
+
+int launch_sweep_phase(int kind, const CsrArgs& A, const int32_t* rows, int32_t nrows, const double* b, double* x,
+                       int vec, void* stream) {
+  if (nrows <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int threads = 256, rpb = (threads / 32) * (32 / vec);
+  const int grid = (int)std::min<int64_t>(((int64_t)nrows + rpb - 1) / rpb, 148 * 16);
+#define SWEEP_CASE(VV)                                                                     \
+  case VV:                                                                                 \
+    if (kind == 1) k_sweep<1, VV><<<grid, threads, 0, st>>>(A, rows, nrows, b, x);          \
+    else k_sweep<2, VV><<<grid, threads, 0, st>>>(A, rows, nrows, b, x);                    \
+    break;
+  switch (vec) {
+    SWEEP_CASE(1)
+    SWEEP_CASE(2)
+    SWEEP_CASE(4)
+    SWEEP_CASE(8)
+    SWEEP_CASE(16)
+    default:
+      if (kind == 1) k_sweep<1, 32><<<grid, threads, 0, st>>>(A, rows, nrows, b, x);
+      else k_sweep<2, 32><<<grid, threads, 0, st>>>(A, rows, nrows, b, x);
+  }
+#undef SWEEP_CASE
   return (int)cudaGetLastError();
 }
 

@@ -282,3 +282,58 @@ def test_rcm_vs_scipy(mk):
     root = int(ref[-1])
     assert np.diff(gp)[root] == np.diff(gp).min()
     assert rcm_order(gp, ga, [root]) == list(ref)
+
+
+# ------------------------------------------------------- NEXT-4 sweep pins
+def _spd_small():
+    U = gen.random_symmetric(40, 5.0, 3)
+    A = oracle.to_dense(U)
+    # diagonally dominant SPD: GS and Kaczmarz converge, A^{-1} b is unique
+    U = gen.from_edges(40, *np.nonzero(np.triu(A, 1)), A[np.triu_indices(40, 1)][np.triu(A, 1)[np.triu_indices(40, 1)] != 0],
+                       np.abs(A).sum(1) + 1.0)
+    return U
+
+
+def test_gs_sweep_is_the_matrix_splitting():
+    """One forward GS sweep in natural order is x' = (D + L)^{-1} (b - U_s x)
+    (textbook splitting A = L + D + U_s; numpy triangular solve)."""
+    import scipy.linalg as sl
+    U = _spd_small()
+    A = oracle.to_dense(U)
+    rng = np.random.default_rng(1)
+    b, x0 = rng.uniform(-1, 1, U.n), rng.uniform(-1, 1, U.n)
+    x = oracle.sweep("gs", U, b, x0, np.arange(U.n, dtype=np.int32))
+    ref = sl.solve_triangular(np.tril(A), b - np.triu(A, 1) @ x0, lower=True)
+    assert relinf(x, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("kind", ["gs", "kacz"])
+def test_sweeps_fix_the_solution_and_converge(kind):
+    """A x* = b is a fixed point of both sweeps; symmetric sweeps converge to it."""
+    U = _spd_small()
+    A = oracle.to_dense(U)
+    rng = np.random.default_rng(2)
+    b = rng.uniform(-1, 1, U.n)
+    xs = np.linalg.solve(A, b)
+    order = rng.permutation(U.n).astype(np.int32)
+    assert relinf(oracle.sweep(kind, U, b, xs, order, symmetric=True), xs) <= 1e-13
+    x = np.zeros(U.n)
+    res = []
+    for _ in range(30):
+        x = oracle.sweep(kind, U, b, x, order, symmetric=True)
+        res.append(np.linalg.norm(A @ x - b))
+    assert res[-1] < 1e-3 * res[0] and res[-1] <= np.linalg.norm(b) * 1e-4
+
+
+def test_kacz_projects_onto_the_row():
+    """eq:KACZ: after projecting onto row i, <A_i, x> = b_i,
+    and x moved along A_i only."""
+    U = _spd_small()
+    A = oracle.to_dense(U)
+    rng = np.random.default_rng(3)
+    b, x0 = rng.uniform(-1, 1, U.n), rng.uniform(-1, 1, U.n)
+    for i in (0, 7, 39):
+        x = oracle.sweep("kacz", U, b, x0, np.array([i], dtype=np.int32))
+        assert abs(A[i] @ x - b[i]) <= 1e-13 * (np.abs(A[i]) @ np.abs(x) + abs(b[i]))
+        d = x - x0
+        assert np.allclose(d, (d @ A[i]) / (A[i] @ A[i]) * A[i], atol=1e-14)
