@@ -463,6 +463,21 @@ def main():
 
     variant = a.variant if a.variant != "auto" else "tiled_atomic"  # what AUTO runs (symmspmv.h)
     ms_step, launches, clocks = timed(variant, a.steps, max(3, a.warmup))
+
+    # per-step distribution (mean, median, min/max spread, flag > 5%),
+    # from a separate pass with one event per step (not the timed number)
+    nst = max(10, min(a.steps, 200))
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)]
+    evs[0].record(stream)
+    for i in range(nst):
+        step(i, variant)
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(nst)])
+    med = float(np.median(per))
+    step_stats = {"steps": nst, "mean_ms": float(per.mean()), "median_ms": med, "min_ms": float(per.min()),
+                  "max_ms": float(per.max()), "spread": float((per.max() - per.min()) / med),
+                  "spread_over_5pct": bool((per.max() - per.min()) / med > 0.05)}
     t_s = ms_step / 1e3
     gflops_rank = 2.0 * nf / t_s / 1e9
     value = gflops_rank * ws  # replicas: every rank multiplies its own copy
@@ -516,7 +531,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": a.steps, "warmup": max(3, a.warmup),
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "ours", "variant": variant, "gpu_launches": launches,
+        "data": "synthetic", "impl": "ours", "variant": variant, "gpu_launches": launches, "step_stats": step_stats,
         "config": {"workload": a.config, "n": n, "nnz_upper": int(U.nnz), "nnz_full": nf,
                    "parallelism": f"replicas{ws}" if ws > 1 else "single",
                    "l2_policy": f"inputs larger than L2: matrix {dev_bytes / 1e6:.0f} MB streamed per step; "
