@@ -259,6 +259,8 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
   double gain = 0.25;
   if (const char* v = std::getenv("SYMM_SORT_GAIN")) gain = std::atof(v);
   std::vector<char> sort_tile((size_t)nt, 0);
+  const bool place_peel = !std::getenv("SYMM_PLACE_PEEL") || std::atoi(std::getenv("SYMM_PLACE_PEEL")) != 0;
+  const bool peel_sorted = std::getenv("SYMM_PEEL_SORTED") && std::atoi(std::getenv("SYMM_PEEL_SORTED")) != 0;
   std::vector<int64_t> lane_off((size_t)nt + 1, 0);
   for (int32_t t = 0; t < nt; ++t)
     lane_off[(size_t)t + 1] = lane_off[(size_t)t] + (S.tile_ptr[(size_t)t + 1] - S.tile_ptr[(size_t)t]) +
@@ -294,6 +296,10 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     // warp the segment starts are distinct mod 16: the lanes' lock-step val
     // loads then hit distinct bank pairs (pad entries where no row fits)
     int32_t cur = 0, pads = 0;
+    // nvcc's unroll-by-4 of the row loop runs a row's len % 4 leftover steps
+    // first, so a lane's unrolled steps start at entry start + len % 4
+    // (SYMM_PLACE_PEEL=0: plain starts)
+    auto peel = [&](int32_t len) { return place_peel ? (len & 3) : 0; };
     for (int32_t g0 = 0; g0 < W; g0 += 32) {
       std::vector<int32_t> rem;  // lanes of this warp with a row segment
       for (int32_t i = g0; i < std::min(W, g0 + 32); ++i)
@@ -302,17 +308,18 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
       int nrem[2] = {0, 0};
       for (int32_t i : rem) nrem[(i - g0) >> 4]++;
       while (!rem.empty()) {
-        const int32_t r = cur & 15;
-        int best = -1, bsc = -1;
+        int best = -1, bsc = -1, bkey = 0;
         for (size_t q = 0; q < rem.size(); ++q) {
           const int h = (rem[q] - g0) >> 4;
-          if ((used[h] >> r) & 1) continue;
           const int32_t len = S.prow_ptr[(size_t)(r0 + sa[rem[q]]) + 1] - S.prow_ptr[(size_t)(r0 + sa[rem[q]])];
+          // sorted tiles unroll one list of row + transposed entries per lane
+          const int32_t key = (cur + (sort_tile[(size_t)t] ? (peel_sorted ? peel(work[(size_t)sa[rem[q]]]) : 0) : peel(len))) & 15;
+          if ((used[h] >> key) & 1) continue;
           const int32_t er = (cur + len) & 15;
           int sc = 0;  // halves that can still use the residue this row ends on
           for (int h2 = 0; h2 < 2; ++h2)
-            if (nrem[h2] - (h2 == h) > 0 && !((used[h2] | (h2 == h ? 1u << r : 0u)) >> er & 1)) ++sc;
-          if (sc > bsc) { bsc = sc; best = (int)q; }
+            if (nrem[h2] - (h2 == h) > 0 && !((used[h2] | (h2 == h ? 1u << key : 0u)) >> er & 1)) ++sc;
+          if (sc > bsc) { bsc = sc; best = (int)q; bkey = key; }
         }
         if (best < 0) { ++cur; ++pads; continue; }  // no row can start here: pad entry
         const int32_t i = rem[(size_t)best];
@@ -320,7 +327,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         const int32_t row = r0 + sa[i];
         vstart[(size_t)row] = cur;
         cur += S.prow_ptr[(size_t)row + 1] - S.prow_ptr[(size_t)row];
-        used[h] |= 1u << r;
+        used[h] |= 1u << bkey;
         nrem[h]--;
         rem.erase(rem.begin() + best);
       }
@@ -348,7 +355,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     int64_t cap0 = 0;
     for (int32_t t = 0; t < nt; ++t) cap0 = std::max(cap0, block_size(t, 0));
     for (int32_t t = 0; t < nt; ++t)
-      if (tile_pads[(size_t)t] > 0 && block_size(t, tile_pads[(size_t)t]) > cap0) {
+      if (tile_pads[(size_t)t] > 0 && (block_size(t, tile_pads[(size_t)t]) > cap0 || std::getenv("SYMM_NO_PLACE"))) {
         const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1];
         for (int32_t r = r0; r < r1; ++r) vstart[(size_t)r] = S.prow_ptr[(size_t)r] - S.prow_ptr[(size_t)r0];
         tile_pads[(size_t)t] = 0;
@@ -463,6 +470,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
       uint16_t* sid = reinterpret_cast<uint16_t*>(blk + D.o_sid);
       for (int32_t i = 0; i < W; ++i) sid[i] = (uint16_t)slot_at[(size_t)i];
     }
+    const bool uni = D.sorted != 0;  // sorted tiles: one list (row part, then transposed part) per lane
     // row part: a warp walks the lists of 32 consecutive lane positions in
     // lock step; order every row's entries so that at each step the x
     // gathers of a half warp hit distinct bank pairs (window id mod 16)
@@ -476,7 +484,19 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         for (int32_t k = S.prow_ptr[(size_t)(r0 + l)]; k < S.prow_ptr[(size_t)(r0 + l) + 1]; ++k)
           ent[(size_t)(i - g0)].push_back({(uint16_t)eloc[(size_t)(k - e0)], S.pval[(size_t)k]});
       }
-      if (bank_aware) bank_order_rows(ent, 1);
+      if (bank_aware) {
+        bank_order_rows(ent, 1);
+        // the unrolled loop runs a lane's n % 4 leftover steps first (n = its
+        // loop length): the matched order is for the steps after them, so the
+        // entries matched last become the leftover (first) entries
+        for (int32_t i = g0; i < g1; ++i) {
+          const int32_t l = slot_at[(size_t)i];
+          if (l >= T || !place_peel) continue;
+          auto& e = ent[(size_t)(i - g0)];
+          const int32_t off = uni && !peel_sorted ? 0 : std::min<int32_t>((int32_t)e.size(), (uni ? rl[(size_t)l] + cl[(size_t)l] : rl[(size_t)l]) & 3);
+          std::rotate(e.begin(), e.end() - off, e.end());
+        }
+      }
       for (int32_t i = g0; i < g1; ++i) {
         const int32_t l = slot_at[(size_t)i];
         if (l >= T) continue;
@@ -499,17 +519,26 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     const int32_t vb = (int32_t)(D.o_val / 8);  // bank-pair phase of val[0]
     // sorted tiles walk one list per lane (row part, then transposed part) in
     // lock step; unsorted tiles walk the two parts as separate lock-step loops
-    const bool uni = D.sorted != 0;
     auto rlen = [&](int32_t l) { return (uni && l < T) ? rl[(size_t)l] : 0; };
     if (bank_aware)
       for (int32_t g0 = 0; g0 < W; g0 += 32) {
         const int32_t g1 = std::min(W, g0 + 32);
-        int32_t maxlen = 0;
+        // execution steps of the warp's unrolled loop: first the lanes' n % 4
+        // leftover steps (P = the largest), then the blocks of 4 in lock step;
+        // lane i is at list index idx(tau) (n = its loop length)
+        int32_t nn[32], off[32], P = 0, tmax = 0;
         for (int32_t i = g0; i < g1; ++i) {
           const int32_t l = slot_at[(size_t)i];
-          maxlen = std::max(maxlen, rlen(l) + (int32_t)lists[(size_t)l].size());
+          nn[i - g0] = rlen(l) + (int32_t)lists[(size_t)l].size();
+          off[i - g0] = place_peel && (!uni || peel_sorted) ? (nn[i - g0] & 3) : 0;
+          P = std::max(P, off[i - g0]);
         }
-        for (int32_t j = 0; j < maxlen; ++j)
+        for (int32_t i = g0; i < g1; ++i) tmax = std::max(tmax, P + nn[i - g0] - off[i - g0]);
+        auto idx_at = [&](int32_t i, int32_t tau) -> int32_t {
+          const int32_t v = tau < P ? (tau < off[i - g0] ? tau : -1) : off[i - g0] + (tau - P);
+          return v < nn[i - g0] ? v : -1;
+        };
+        for (int32_t tau = 0; tau < tmax; ++tau)
           for (int32_t h = g0; h < g1; h += 16) {
             const int32_t h1 = std::min(g1, h + 16);
             // bank-pair load counts of this (step, half warp): lanes still in
@@ -517,21 +546,24 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
             // one of its remaining entries.  Several greedy passes (lane orders)
             // minimise max val load + max x load (= wavefronts of the 2 loads).
             int cv0[16] = {0}, cr0[16] = {0};
-            int act[16], na = 0;
+            int act[16], actj[16], na = 0;
             for (int32_t i = h; i < h1; ++i) {
               const int32_t l = slot_at[(size_t)i];
-              if (j < rlen(l)) {
-                const int32_t k = rst[(size_t)l] + j;
+              const int32_t v = idx_at(i, tau);
+              if (v < 0) continue;
+              if (v < rlen(l)) {
+                const int32_t k = rst[(size_t)l] + v;
                 cv0[(k + vb) & 15]++;
                 cr0[lcol[k] & 15]++;
+              } else {
+                act[na] = i;
+                actj[na++] = v - rlen(l);
               }
-              const int32_t jj = j - rlen(l);
-              if (jj >= 0 && jj < (int32_t)lists[(size_t)l].size()) act[na++] = i;
             }
             if (na == 0) continue;
             int best_cost = INT32_MAX;
             size_t best_pick[16], pick[16];
-            uint32_t rs = 0x9e3779b9u ^ (uint32_t)(j * 131 + h);
+            uint32_t rs = 0x9e3779b9u ^ (uint32_t)(tau * 131 + h);
             for (int pass = 0; pass < csc_passes; ++pass) {
               int ord[16];
               for (int q = 0; q < na; ++q) ord[q] = q;
@@ -546,7 +578,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
               for (int q = 0; q < na; ++q) {
                 const int32_t l = slot_at[(size_t)act[ord[q]]];
                 const auto& L = lists[(size_t)l];
-                const size_t jj = (size_t)(j - rlen(l));
+                const size_t jj = (size_t)actj[ord[q]];
                 size_t bq = jj;
                 int bsc = INT32_MAX;
                 for (size_t e = jj; e < L.size(); ++e) {
@@ -565,9 +597,8 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
               }
             }
             for (int q = 0; q < na; ++q) {
-              const int32_t l = slot_at[(size_t)act[q]];
-              auto& L = lists[(size_t)l];
-              std::swap(L[(size_t)(j - rlen(l))], L[best_pick[q]]);
+              auto& L = lists[(size_t)slot_at[(size_t)act[q]]];
+              std::swap(L[(size_t)actj[q]], L[best_pick[q]]);
             }
           }
       }

@@ -85,10 +85,13 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
             assert np.array_equal(gid[w:w + ln], g + np.arange(ln))
             if int(D["gather_runs"]):
                 assert (w - (g - row0)) % 2 == 0
-        if nnz > int(rln.sum()):  # padded placement: rows of a half warp start on distinct bank pairs
+        if nnz > int(rln.sum()):  # padded placement: the unrolled steps of a half warp's rows
+            # (which begin after each lane's loop-length % 4 leftover steps) start on distinct bank pairs
             for g0 in range(0, W, 16):
-                ls = [int(sid[i]) for i in range(g0, min(W, g0 + 16)) if sid[i] < T]
-                res = [(int(D["o_val"]) // 8 + int(rst[l])) % 16 for l in ls]
+                idx = [i for i in range(g0, min(W, g0 + 16)) if sid[i] < T]
+                n_loop = [int(rln[sid[i]]) + (int(tptr[i + 1] - tptr[i]) if int(D["sorted"]) else 0) for i in idx]
+                res = [(int(D["o_val"]) // 8 + int(rst[sid[i]]) + (0 if int(D["sorted"]) else nl & 3)) % 16
+                       for i, nl in zip(idx, n_loop)]
                 assert len(set(res)) == len(res)
         for i in range(W):
             l = int(sid[i])
