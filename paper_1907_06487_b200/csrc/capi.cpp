@@ -526,17 +526,28 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         // execution steps of the warp's unrolled loop: first the lanes' n % 4
         // leftover steps (P = the largest), then the blocks of 4 in lock step;
         // lane i is at list index idx(tau) (n = its loop length)
-        int32_t nn[32], off[32], P = 0, tmax = 0;
+        // (sorted tiles' unified loop: blocks of 4 first, then the leftover
+        // steps of every lane together: lane i at 4 (n_i / 4) + t)
+        int32_t nn[32], off[32], P = 0, tmax = 0, B4 = 0;
+        const bool rem_last = uni && !peel_sorted && place_peel;
         for (int32_t i = g0; i < g1; ++i) {
           const int32_t l = slot_at[(size_t)i];
           nn[i - g0] = rlen(l) + (int32_t)lists[(size_t)l].size();
           off[i - g0] = place_peel && (!uni || peel_sorted) ? (nn[i - g0] & 3) : 0;
           P = std::max(P, off[i - g0]);
+          B4 = std::max(B4, nn[i - g0] & ~3);
         }
-        for (int32_t i = g0; i < g1; ++i) tmax = std::max(tmax, P + nn[i - g0] - off[i - g0]);
+        for (int32_t i = g0; i < g1; ++i)
+          tmax = std::max(tmax, rem_last ? B4 + (nn[i - g0] & 3) : P + nn[i - g0] - off[i - g0]);
         auto idx_at = [&](int32_t i, int32_t tau) -> int32_t {
+          const int32_t n = nn[i - g0];
+          if (rem_last) {
+            if (tau < B4) return tau < (n & ~3) ? tau : -1;
+            const int32_t t = tau - B4;
+            return t < (n & 3) ? (n & ~3) + t : -1;
+          }
           const int32_t v = tau < P ? (tau < off[i - g0] ? tau : -1) : off[i - g0] + (tau - P);
-          return v < nn[i - g0] ? v : -1;
+          return v < n ? v : -1;
         };
         for (int32_t tau = 0; tau < tmax; ++tau)
           for (int32_t h = g0; h < g1; h += 16) {
