@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="st27_128")
-    ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "tree", "auto"])
+    ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "tree", "tiled_colored", "auto"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sweep", default=None, choices=["gs", "kacz"],
                     help="NEXT-4: time symmetric Gauss-Seidel / Kaczmarz sweeps instead of SymmSpMV (own JSON line)")

@@ -167,6 +167,12 @@ typedef enum {
   SYMM_VARIANT_SPMV = 6,        /* the paper's yardstick (Alg. 1): the same y := A x
                                    from the FULL matrix A = U + U^T - diag(U) in CRS, the plan
                                    mirrors U; deterministic, no atomics   */
+  SYMM_VARIANT_TILED_COLORED = 8,/* K8: the K4 tiles in one launch, processed phase by phase
+                                   (phase-major order); a tile flushes its window after its
+                                   DAG predecessors (conflicting tiles of earlier phases) have:
+                                   the first writer of a row stores, later writers add in phase
+                                   order.  No atomics, no zeroing of y, deterministic; the
+                                   colored scheme at streaming speed        */
   SYMM_VARIANT_TREE = 7         /* K7: the recursive RACE tree (schedule scheme 3 only, else
                                    SYMM_ERR_ARG) in one persistent launch: one CTA per leaf at a
                                    time, leaves claimed in red-before-blue depth-first order,

@@ -8,7 +8,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsymmspmv
 
 SYMM_ORDER_PERMUTED = 0
 SYMM_ORDER_ORIGINAL = 1
-VARIANTS = {"auto": 0, "colored": 1, "atomic": 2, "tiled": 3, "tiled_atomic": 4, "colored_smem": 5, "spmv": 6, "tree": 7}
+VARIANTS = {"auto": 0, "colored": 1, "atomic": 2, "tiled": 3, "tiled_atomic": 4, "colored_smem": 5, "spmv": 6, "tree": 7, "tiled_colored": 8}
 
 
 class SymmError(RuntimeError):

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <numeric>
 #include <string>
 #include <vector>
 
@@ -61,6 +62,8 @@ struct symmspmv_plan {
   int tiled_occ = 0;
   int32_t* d_in_ptr = nullptr;
   FixupArgs fargs{};
+  // K8 tiled_colored
+  bool has_tiled_colored = false;
   // K7 recursive tree
   bool has_tree = false;
   TreeArgs tree{};
@@ -231,6 +234,8 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     run_ptr[(size_t)t + 1] = run_ptr[(size_t)t] + nr;
   }
   std::vector<int32_t> slot_tgt((size_t)slot_ptr[(size_t)nt], -1);
+  std::vector<char> slot_first((size_t)slot_ptr[(size_t)nt], 0);  // this tile writes the target first (lowest phase)
+  if (n >= kTgtFirst) return set_error(SYMM_ERR_UNSUPPORTED, "tiled format: n >= 2^30");
 
   std::vector<SpillRun> runs((size_t)run_ptr[(size_t)nt]);
 #pragma omp parallel for schedule(dynamic, 64)
@@ -248,6 +253,17 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
       slot_tgt[(size_t)(slot_ptr[(size_t)t] + w)] = g;
       ++w;
       prev = g;
+    }
+  }
+  // K8 (tiled_colored): the first writer of a row (the writer tile of the
+  // lowest phase, schedule.cpp) stores, the others add after it in phase order
+  for (int32_t t = 0; t < nt; ++t) {
+    int64_t w = slot_ptr[(size_t)t];
+    for (int64_t q = S.spill_ptr[(size_t)t]; q < S.spill_ptr[(size_t)t + 1]; ++q) {
+      const int32_t g = (int32_t)((uint32_t)S.spill[(size_t)q] & kIdxMask);
+      while (slot_tgt[(size_t)w] != g) ++w;  // pads (-1) between runs
+      slot_first[(size_t)w] = ((uint32_t)S.spill[(size_t)q] & kFirstBit) != 0;
+      ++w;
     }
   }
   // Per tile: lane positions in slot order, or sorted by descending work
@@ -439,7 +455,9 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
     const int32_t* st = slot_tgt.data() + slot_ptr[(size_t)t];
-    for (int32_t j = 0; j < ns; ++j) tgt[j] = st[j];  // flush target of every spill slot (-1 = pad)
+    // flush target of every spill slot (-1 = pad), bit 30 = first writer
+    for (int32_t j = 0; j < ns; ++j)
+      tgt[j] = st[j] < 0 ? st[j] : (st[j] | (slot_first[(size_t)(slot_ptr[(size_t)t] + j)] ? kTgtFirst : 0));
     const int32_t e0 = S.prow_ptr[(size_t)r0];
     const SpillRun* tr = runs.data() + run_ptr[(size_t)t];
     const int32_t nrt = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
@@ -464,7 +482,8 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     std::vector<int32_t> rst((size_t)std::max(T, 1), 0);
     for (int32_t l = 0; l < T; ++l) {
       rst[(size_t)l] = vstart[(size_t)(r0 + l)];
-      rseg[l] = (uint32_t)rst[(size_t)l] | ((uint32_t)rl[(size_t)l] << 16);
+      rseg[l] = (uint32_t)rst[(size_t)l] | ((uint32_t)rl[(size_t)l] << 16) |
+                (S.own_first[(size_t)(r0 + l)] ? kRsegFirst : 0u);
     }
     if (D.sorted) {
       uint16_t* sid = reinterpret_cast<uint16_t*>(blk + D.o_sid);
@@ -662,6 +681,28 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
       (rc = upload(P, &d_slots, H.slots.data(), H.slots.size())) || (rc = upload(P, &d_runs, H.runs.data(), H.runs.size())) ||
       (rc = upload(P, &P->d_in_ptr, H.in_ptr.data(), H.in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
     return rc;
+  if (t_begin == 0 && t_end == (int32_t)S.tile_group.size()) {
+    // K8 (single rank): tiles in id order, DAG of smaller-id writers, flush counters
+    // phase-major order (phases are the tile colours: the DAG of conflicting
+    // earlier-phase tiles is only n_phases deep)
+    std::vector<int32_t> order((size_t)ntl);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return S.tile_phase[(size_t)a] < S.tile_phase[(size_t)b]; });
+    std::vector<int32_t> dq(S.dag_pred);
+    if (dq.empty()) dq.push_back(0);
+    int32_t *d_order, *d_dp, *d_dq;
+    unsigned int* d_done;
+    if ((rc = upload(P, &d_order, order.data(), order.size())) ||
+        (rc = upload(P, &d_dp, S.dag_ptr.data(), S.dag_ptr.size())) ||
+        (rc = upload(P, &d_dq, dq.data(), dq.size())) || (rc = dev_alloc(P, &d_done, (size_t)std::max(ntl, 1))))
+      return rc;
+    P->targs.order = d_order;
+    P->targs.dag_ptr = d_dp;
+    P->targs.dag_pred = d_dq;
+    P->targs.done = d_done;
+    P->has_tiled_colored = true;
+  }
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
   A.ntiles = ntl;
@@ -912,7 +953,7 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     }
   } else if (variant == SYMM_VARIANT_TILED) {
     if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED was not uploaded by this plan");
-    if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, false, st))) return cuda_fail((cudaError_t)rc, "k_tiled");
+    if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, 0, st))) return cuda_fail((cudaError_t)rc, "k_tiled");
     if ((rc = launch_fixup(P->fargs, y, st))) return cuda_fail((cudaError_t)rc, "k_fixup");
     P->last_launches = 2;
   } else if (variant == SYMM_VARIANT_TILED_ATOMIC) {
@@ -920,9 +961,15 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     // x, y cover rows [row_begin, local_end); kernels index by global row id
     const int64_t nloc = (int64_t)P->local_end - P->row_begin;
     if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
-    if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, true, st)))
+    if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, 1, st)))
       return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
     P->last_launches = 2;
+  } else if (variant == SYMM_VARIANT_TILED_COLORED) {
+    if (!P->has_tiled_colored) return set_error(SYMM_ERR_ARG, "variant TILED_COLORED was not uploaded by this plan");
+    cudaError_t e = cudaMemsetAsync(P->targs.done, 0, sizeof(unsigned int) * (size_t)P->targs.ntiles, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tile counters");
+    if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, 2, st))) return cuda_fail((cudaError_t)rc, "k_tiled<ordered>");
+    P->last_launches = 1;
   } else if (variant == SYMM_VARIANT_TREE) {
     if (!P->has_tree) return set_error(SYMM_ERR_ARG, "variant TREE was not uploaded by this plan");
     CsrArgs A{P->n, P->d_rp, P->d_col, P->d_val};
@@ -1123,7 +1170,7 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   if (U && (U->n != S.n || U->nnz != S.nnz))
     return set_error(SYMM_ERR_MISMATCH, "matrix (n=%d, nnz=%lld) does not match the schedule (n=%d, nnz=%lld)", U->n,
                      (long long)U->nnz, S.n, (long long)S.nnz);
-  if (opt.variant < 0 || opt.variant > 7) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
+  if (opt.variant < 0 || opt.variant > 8) return set_error(SYMM_ERR_ARG, "variant %d", opt.variant);
   if (opt.nranks < 1 || opt.rank < 0 || opt.rank >= opt.nranks)
     return set_error(SYMM_ERR_ARG, "rank %d of %d", opt.rank, opt.nranks);
   if (opt.nranks > 1 && opt.variant != SYMM_VARIANT_TILED_ATOMIC && opt.variant != SYMM_VARIANT_AUTO)
@@ -1159,7 +1206,8 @@ int symmspmv_plan(const race_schedule_t* s, const symm_csr_upper* U, const symms
   int rc = SYMM_OK;
   const bool all = opt.build_all != 0;
   const int v = opt.variant;
-  bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_TILED_ATOMIC || v == SYMM_VARIANT_AUTO;
+  bool want_tiled = all || v == SYMM_VARIANT_TILED || v == SYMM_VARIANT_TILED_ATOMIC || v == SYMM_VARIANT_AUTO ||
+                    v == SYMM_VARIANT_TILED_COLORED;
   bool want_col = all || v == SYMM_VARIANT_COLORED;
   bool want_csr = all || v == SYMM_VARIANT_ATOMIC || v == SYMM_VARIANT_COLORED;
   bool want_cs = all || v == SYMM_VARIANT_COLORED_SMEM;
@@ -1336,7 +1384,7 @@ extern "C" int symmspmv_debug_trace(symmspmv_plan_t* P, const double* x, double*
   cudaMemset(d, 0, bytes);
   TiledArgs A = P->targs;
   A.trace = d;
-  int rc = launch_tiled(A, x, y, P->vec, P->tiled_grid, false, stream);
+  int rc = launch_tiled(A, x, y, P->vec, P->tiled_grid, 0, stream);
   cudaStreamSynchronize((cudaStream_t)stream);
   cudaMemcpy(host_trace, d, bytes, cudaMemcpyDeviceToHost);
   cudaFree(d);

@@ -130,7 +130,17 @@ struct TiledArgs {
   unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
   int32_t debug_skip;             // diagnostics only (env SYMM_DEBUG_SKIP): skip bit0 row part,
                                   // bit1 CSC part, bit2 flush, bit3 spill-x gather (wrong results)
+  // K8 (tiled_colored, MODE 2): tiles processed in phase-major order; a tile
+  // flushes after its DAG predecessors (conflicting tiles of earlier phases)
+  const int32_t* order;           // [ntiles] processing order -> tile id
+  const int32_t* dag_ptr;         // [ntiles+1] predecessors of every tile id
+  const int32_t* dag_pred;
+  unsigned int* done;             // [ntiles] warps of the owning group that flushed (zeroed per run)
 };
+// first-writer flags inside the tile block (K8 stores instead of adding):
+// rseg bit 31 (own row), tgt bit 30 (spill slot); K3/K4 mask them off
+constexpr uint32_t kRsegFirst = 0x80000000u;
+constexpr int32_t kTgtFirst = 0x40000000;
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions
   int32_t n;
@@ -245,7 +255,7 @@ int launch_zero(double* y, int64_t n, void* stream);
 int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms, void* stream);
 int launch_colored_phase(const CsrArgs& A, const ColoredArgs& C, const double* x, double* y, int vec,
                          void* stream);
-int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream);
+int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, int mode, void* stream);
 int launch_fixup(const FixupArgs& F, double* y, void* stream);
 int tiled_smem_bytes(const TiledArgs& T);
 int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);  // returns the ring depth in *out

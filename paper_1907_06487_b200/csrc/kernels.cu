@@ -365,9 +365,14 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
 }
 
-template <bool ATOMIC, int NS>
+// MODE 0: K3 (own rows stored, spill staged for k_fixup), 1: K4 (fp64 RED
+// into zeroed y), 2: K8 (phase-major order, DAG-ordered store / add: no
+// atomics, no zeroing, deterministic)
+template <int MODE, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
+  constexpr bool ATOMIC = MODE == 1;
+  constexpr bool ORDERED = MODE == 2;
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t blk_full[NS], x_full[NS], empty[NS];
   __shared__ int loader_k;  // tiles the loader has taken a free stage for (gather warps follow it)
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       auto ld = [&](int kk, int4& d, int& T) {
         const int tt = blockIdx.x + kk * G;
         if (tt < A.ntiles) {
-          const TileDesc& D = A.tiles[tt];
+          const TileDesc& D = A.tiles[ORDERED ? __ldg(A.order + tt) : tt];
           const int64_t o = D.block_off;
           d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
           T = D.nrows;
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     int k = gw;
     for (int t = blockIdx.x + gw * G; t < A.ntiles; t += kGatherWarps * G, k += kGatherWarps) {
       const int s = k % NS;
-      const TileDesc* Dg = A.tiles + t;
+      const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(A.order + t) : t);
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
       const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
       const int gruns = __ldg(&Dg->gather_runs) && !(A.debug_skip & 8);
@@ -530,7 +535,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int S = D.nspill;
 #pragma unroll 4
         for (int idx = lane; idx < S; idx += 32) {
-          const int g = tgt[idx];
+          const int g = tgt[idx] & ~kTgtFirst;  // (-1 pads stay negative)
 #ifdef K4_CHECK
           if (g >= A.check_n || T + idx + p >= A.window_cap) { printf("K4_CHECK loose t=%d g=%d idx=%d\n", t, g, idx); __trap(); }
 #endif
@@ -576,11 +581,41 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // flush of window slot l: K4 one RED per (tile, target); K3 own rows
     // stored, spill contributions staged
+    // K8: before its first store / add, a warp waits until every DAG
+    // predecessor of the tile (a conflicting tile of an earlier phase) has
+    // been flushed by all the warps of its group
+    // K8: before its first store / add, a warp waits until every DAG
+    // predecessor of the tile (a conflicting tile of an earlier phase) has
+    // been flushed by all the warps of its group
+    const int tile_id = ORDERED ? __ldg(A.order + t) : t;
+    if (ORDERED && !(A.debug_skip & 16)) {  // (bit 4: diagnostics, no DAG wait)
+      const int pb = __ldg(A.dag_ptr + tile_id), pe = __ldg(A.dag_ptr + tile_id + 1);
+      for (int q = pb + lane; q < pe; q += 32) {
+        const unsigned* f = A.done + __ldg(A.dag_pred + q);
+        while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(64);
+      }
+      __syncwarp();
+      __threadfence();
+    }
     auto flush = [&](int l, int sl, double acc) {
       if (A.debug_skip & 4) {
         // diagnostics: no flush
+      } else if (ORDERED) {
+        // first writer of the target (lowest phase) stores, later ones add in
+        // phase order (the DAG): y needs no zeroing and no atomics
+        bool first;
+        int gr;
+        if (l < T) {
+          gr = row0 + l;
+          first = (rseg[l] & kRsegFirst) != 0;
+        } else {
+          const int tv = tgt[l - T];
+          gr = tv < 0 ? -1 : (tv & ~kTgtFirst);
+          first = tv >= 0 && (tv & kTgtFirst) != 0;
+        }
+        if (gr >= 0) __stcg(y + gr, (first || (A.debug_skip & 32)) ? acc : __ldcg(y + gr) + acc);  // (bit 5: no RMW)
       } else if (ATOMIC) {
-        const int gr = l < T ? row0 + l : tgt[l - T];
+        const int gr = l < T ? row0 + l : (tgt[l - T] & ~kTgtFirst);
 #ifdef K4_CHECK
         if (gr >= A.check_n) { printf("K4_CHECK flush t=%d l=%d gr=%d\n", t, l, gr); __trap(); }
 #endif
@@ -604,7 +639,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         double acc = 0.0;
         if (l < T && !(A.debug_skip & 1)) {
           const uint32_t sg = rseg[l];
-          const int eb = (int)(sg & 0xffffu), ee = eb + (int)(sg >> 16);
+          const int eb = (int)(sg & 0xffffu), ee = eb + (int)((sg >> 16) & 0x7fffu);
 #pragma unroll 4
           for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
         }
@@ -627,7 +662,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         if (l < T && !(A.debug_skip & 1)) {
           const uint32_t sg = rseg[l];
           eb = (int)(sg & 0xffffu);
-          nr = (int)(sg >> 16);
+          nr = (int)((sg >> 16) & 0x7fffu);
         }
         const int jb = tptr[i];
         const int nt = nr + ((A.debug_skip & 2) ? 0 : tptr[i + 1] - jb);
@@ -644,6 +679,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       }
     }
     if (gt == 0) TRACE(k, 4);
+    if (ORDERED) {  // this warp's stores of the tile are visible: count it
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(A.done + tile_id, 1u);
+    }
     // release stage s: each warp arrives once its reads of the stage are done
     __syncwarp();
     if (lane == 0) mbar_arrive_relaxed(&empty[s]);
@@ -1096,8 +1136,9 @@ int tiled_smem_bytes(const TiledArgs& T) {
 
 template <int NS>
 static int tiled_attr(int smem) {
-  int rc = (int)cudaFuncSetAttribute(k_tiled<false, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (!rc) rc = (int)cudaFuncSetAttribute(k_tiled<true, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int rc = (int)cudaFuncSetAttribute(k_tiled<0, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (!rc) rc = (int)cudaFuncSetAttribute(k_tiled<1, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (!rc) rc = (int)cudaFuncSetAttribute(k_tiled<2, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   return rc;
 }
 
@@ -1129,7 +1170,7 @@ int tiled_max_ctas_per_sm(int vec, const TiledArgs& T0, int* out) {
   return 0;
 }
 
-int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, bool atomic_flush, void* stream) {
+int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int grid, int mode, void* stream) {
   (void)vec;
   if (T.ntiles <= 0) return 0;
   // programmatic dependent launch: the kernel's loader streams tile blocks
@@ -1146,10 +1187,11 @@ int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int gr
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e = cudaErrorInvalidValue;
-#define LT(NSV)                                                                 \
-  case NSV:                                                                     \
-    e = atomic_flush ? cudaLaunchKernelEx(&cfg, k_tiled<true, NSV>, T, x, y)    \
-                     : cudaLaunchKernelEx(&cfg, k_tiled<false, NSV>, T, x, y);  \
+#define LT(NSV)                                                                                  \
+  case NSV:                                                                                      \
+    e = mode == 1 ? cudaLaunchKernelEx(&cfg, k_tiled<1, NSV>, T, x, y)                           \
+                  : mode == 2 ? cudaLaunchKernelEx(&cfg, k_tiled<2, NSV>, T, x, y)                \
+                              : cudaLaunchKernelEx(&cfg, k_tiled<0, NSV>, T, x, y);               \
     break;
   switch (T.stages) {
     LT(8) LT(6) LT(5) LT(4) LT(3) LT(2)

@@ -15,7 +15,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
-VARIANTS = ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem", "spmv")
+VARIANTS = ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem", "spmv", "tiled_colored")
 # fp64 RED flushes: run-to-run summation order varies (reading R5)
 NONDET = ("atomic", "tiled_atomic", "colored_smem")
 
@@ -162,7 +162,7 @@ def test_parity_full_size(name):
     plan = P.Plan(s, U, variant="auto", build_all=True)
     xd = torch.from_numpy(x[inv].copy()).cuda()
     yd = torch.empty_like(xd)
-    for v in ("tiled", "tiled_atomic", "atomic", "colored_smem", "spmv"):
+    for v in ("tiled", "tiled_atomic", "atomic", "colored_smem", "spmv", "tiled_colored"):
         yd.fill_(float("nan"))
         plan.run(xd, yd, variant=v)
         torch.cuda.synchronize()

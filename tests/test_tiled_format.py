@@ -49,6 +49,7 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
     returns the (row, col) pairs read by row parts and by transposed parts."""
     b = blocks.tobytes()
     y = np.zeros(n, dtype=np.float64)
+    first_count = np.zeros(n, dtype=np.int64)
     row_pairs, csc_pairs = [], []
     for D in desc:
         h = int(D["block_off"])
@@ -57,7 +58,8 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
         T, S, row0, nnz = int(D["nrows"]), int(D["nspill"]), int(D["row0"]), int(D["nnz"])
         W = T + S
         rseg = np.frombuffer(b, dtype="<u4", count=T, offset=h + 64).astype(np.int64)
-        rst, rln = rseg & 0xFFFF, rseg >> 16  # own row segments: [rst, rst + rln)
+        rst, rln = rseg & 0xFFFF, (rseg >> 16) & 0x7FFF  # own row segments: [rst, rst + rln)
+        own_first = (rseg >> 31) & 1                     # K8: this tile writes the row first
         seg = np.zeros(nnz, dtype=np.int64)  # segments are disjoint (pads belong to none)
         for l in range(T):
             seg[rst[l]:rst[l] + rln[l]] += 1
@@ -66,8 +68,14 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
         tptr = np.frombuffer(b, dtype="<u2", count=W + 1, offset=h + int(D["o_tptr"])).astype(np.int64)
         noff = int(tptr[W])
         tcsc = np.frombuffer(b, dtype="<u4", count=noff, offset=h + int(D["o_tidx"])).astype(np.int64)
-        tgt = np.frombuffer(b, dtype="<i4", count=S, offset=h + int(D["o_tgt"])).astype(np.int64)
+        tgt_raw = np.frombuffer(b, dtype="<i4", count=S, offset=h + int(D["o_tgt"])).astype(np.int64)
+        tgt = np.where(tgt_raw < 0, tgt_raw, tgt_raw & ~(1 << 30))
+        spill_first = (tgt_raw >= 0) & ((tgt_raw >> 30) & 1 == 1)
         assert np.array_equal(tgt, targets[int(D["spill_off"]):int(D["spill_off"]) + S])
+        for r in np.nonzero(own_first)[0]:
+            first_count[row0 + r] += 1
+        for g in tgt[spill_first]:
+            first_count[g] += 1
         val = np.frombuffer(b, dtype="<f8", count=nnz, offset=h + int(D["o_val"]))
         if int(D["sorted"]):
             sid = np.frombuffer(b, dtype="<u2", count=W, offset=h + int(D["o_sid"])).astype(np.int64)
@@ -110,6 +118,7 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
                 y[gid[l]] += acc
             else:
                 assert acc == 0.0
+    assert np.all(first_count == 1)  # every row has exactly one first writer (K8 stores, the others add)
     return y, row_pairs, csc_pairs
 
 
