@@ -182,6 +182,7 @@ static int32_t run_local(const SpillRun* tr, int32_t nrt, int32_t r0, int32_t r1
 // K3/K4 format (see TileDesc in internal.h).  Tiles in id (= BFS row) order;
 // a multi-rank plan keeps only its own tile range [t_begin, t_end).
 struct TiledHost {
+  std::vector<char> slot_first;  // K8: spill slot's tile is the target's first writer
   std::vector<TileDesc> desc;
   std::vector<unsigned char> blocks;
   std::vector<int32_t> slot_tgt, slots, in_ptr;
@@ -235,7 +236,6 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
   }
   std::vector<int32_t> slot_tgt((size_t)slot_ptr[(size_t)nt], -1);
   std::vector<char> slot_first((size_t)slot_ptr[(size_t)nt], 0);  // this tile writes the target first (lowest phase)
-  if (n >= kTgtFirst) return set_error(SYMM_ERR_UNSUPPORTED, "tiled format: n >= 2^30");
 
   std::vector<SpillRun> runs((size_t)run_ptr[(size_t)nt]);
 #pragma omp parallel for schedule(dynamic, 64)
@@ -276,14 +276,19 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
   if (const char* v = std::getenv("SYMM_SORT_GAIN")) gain = std::atof(v);
   std::vector<char> sort_tile((size_t)nt, 0);
   const bool place_peel = !std::getenv("SYMM_PLACE_PEEL") || std::atoi(std::getenv("SYMM_PLACE_PEEL")) != 0;
+  // sorted tiles' record loop: blocks of 4 first, leftovers last (measured:
+  // SYMM_PEEL_SORTED=1, the leftovers-first model, is slower)
   const bool peel_sorted = std::getenv("SYMM_PEEL_SORTED") && std::atoi(std::getenv("SYMM_PEEL_SORTED")) != 0;
   std::vector<int64_t> lane_off((size_t)nt + 1, 0);
   for (int32_t t = 0; t < nt; ++t)
     lane_off[(size_t)t + 1] = lane_off[(size_t)t] + (S.tile_ptr[(size_t)t + 1] - S.tile_ptr[(size_t)t]) +
                               (slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
   std::vector<int32_t> lane_slot((size_t)lane_off[(size_t)nt]), vstart((size_t)n, 0), tile_pads((size_t)nt, 0);
-#pragma omp parallel for schedule(dynamic, 64)
-  for (int32_t t = 0; t < nt; ++t) {
+  // sorted tiles: one list of records (val index | x index) per lane position,
+  // at rec[lane_pst[i]], placed so that a warp's lock-step record loads hit
+  // distinct banks
+  std::vector<int32_t> lane_pst((size_t)lane_off[(size_t)nt], 0), rec_pads((size_t)nt, 0);
+  auto plan_tile = [&](int32_t t, bool allow_sort) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
     const int32_t W = T + (int32_t)(slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
     std::vector<int32_t> work((size_t)W, 0);
@@ -302,7 +307,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     };
     std::vector<int32_t> ws(work);
     std::sort(ws.begin(), ws.end(), std::greater<int32_t>());
-    sort_tile[(size_t)t] = W > 32 && (double)steps(ws) <= (1.0 - gain) * (double)steps(work);
+    sort_tile[(size_t)t] = allow_sort && W > 32 && (double)steps(ws) <= (1.0 - gain) * (double)steps(work);
     // lane position -> window slot
     int32_t* sa = lane_slot.data() + lane_off[(size_t)t];
     for (int32_t i = 0; i < W; ++i) sa[i] = i;
@@ -349,29 +354,87 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
       }
     }
     tile_pads[(size_t)t] = pads;
-  }
+    rec_pads[(size_t)t] = 0;
+    if (sort_tile[(size_t)t]) {
+      // record lists: keys (start + leftover steps) distinct mod 32 in a warp
+      int32_t rcur = 0, rp = 0;
+      int32_t* pst = lane_pst.data() + lane_off[(size_t)t];
+      for (int32_t g0 = 0; g0 < W; g0 += 32) {
+        std::vector<int32_t> rem;
+        for (int32_t i = g0; i < std::min(W, g0 + 32); ++i) rem.push_back(i);
+        uint32_t used = 0;
+        while (!rem.empty()) {
+          int best = -1;
+          for (size_t q = 0; q < rem.size(); ++q) {
+            const int32_t nq = work[(size_t)sa[rem[q]]];
+            const int32_t key = (rcur + (peel_sorted ? (nq & 3) : 0)) & 31;
+            if (nq == 0 || !((used >> key) & 1)) { best = (int)q; break; }
+          }
+          if (best < 0) { ++rcur; ++rp; continue; }
+          const int32_t i = rem[(size_t)best];
+          const int32_t nq = work[(size_t)sa[i]];
+          if (nq > 0) used |= 1u << ((rcur + (peel_sorted ? (nq & 3) : 0)) & 31);
+          pst[i] = rcur;
+          rcur += nq;
+          rem.erase(rem.begin() + best);
+        }
+      }
+      rec_pads[(size_t)t] = rp;
+    }
+  };
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int32_t t = 0; t < nt; ++t) plan_tile(t, true);
   // the ring depth follows the largest block: pad entries must not grow it.
   // A tile whose padded block would exceed the largest unpadded block keeps
   // its segments contiguous (no pads; bank-pair starts not guaranteed).
-  auto block_size = [&](int32_t t, int64_t pads) -> int64_t {
+  // block layout of tile t (capi.cpp / internal.h TileDesc); sorted tiles
+  // carry record lists (pseg u32[W] + rec u32) instead of lcol / tcsc / tptr
+  struct Layout { int64_t o_lcol, o_tidx, o_tptr, o_sid, o_tgt, o_val, bytes, nnz, nrec; };
+  auto layout = [&](int32_t t, bool srt, int64_t pads, int64_t rpads) -> Layout {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
     const int64_t S_ = slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t], W = T + S_;
     const int64_t nnz0 = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
     int64_t nd = 0;
     for (int32_t r = r0; r < r1; ++r) nd += (S.prow_ptr[(size_t)r + 1] > S.prow_ptr[(size_t)r] && S.pcol[(size_t)S.prow_ptr[(size_t)r]] == r);
-    int64_t o = align16((int64_t)sizeof(TileDesc) + 4 * (int64_t)T);
-    o = align16(o + 2 * (nnz0 + pads));
-    o = align16(o + 4 * (nnz0 - nd));
-    o = align16(o + 2 * (W + 1));
-    if (sort_tile[(size_t)t]) o = align16(o + 2 * W);
-    o = align16(o + 4 * S_);
-    return align16(o + 8 * (nnz0 + pads));
+    Layout L{};
+    L.nnz = nnz0 + pads;
+    const int64_t o0 = align16((int64_t)sizeof(TileDesc) + 4 * (int64_t)T);  // rseg u32[T]
+    if (!srt) {
+      L.o_lcol = o0;
+      L.o_tidx = align16(L.o_lcol + 2 * L.nnz);
+      L.o_tptr = align16(L.o_tidx + 4 * (nnz0 - nd));
+      L.o_sid = align16(L.o_tptr + 2 * (W + 1));
+      L.o_tgt = L.o_sid;
+    } else {
+      L.nrec = nnz0 + (nnz0 - nd) + rpads;
+      L.o_lcol = o0;                                  // pseg u32[W]: record list of each position
+      L.o_tidx = align16(L.o_lcol + 4 * W);           // rec u32[nrec]: val index | x index << 16
+      L.o_tptr = 0;
+      L.o_sid = align16(L.o_tidx + 4 * L.nrec);
+      L.o_tgt = align16(L.o_sid + 2 * W);
+    }
+    L.o_val = align16(L.o_tgt + 4 * S_);
+    L.bytes = align16(L.o_val + 8 * L.nnz);
+    return L;
   };
   {
-    int64_t cap0 = 0;
-    for (int32_t t = 0; t < nt; ++t) cap0 = std::max(cap0, block_size(t, 0));
+    // pads must not grow the largest block (the ring depth follows it): a
+    // sorted tile whose record format would exceed the largest unpadded
+    // unsorted block is planned unsorted; a padded tile that would exceed it
+    // keeps its row segments contiguous (no pads)
+    int64_t cap0 = 0, maxw = 0;
+    for (int32_t t = 0; t < nt; ++t) {
+      cap0 = std::max(cap0, layout(t, false, 0, 0).bytes);
+      maxw = std::max<int64_t>(maxw, (S.tile_ptr[(size_t)t + 1] - S.tile_ptr[(size_t)t]) + (slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]));
+    }
+    // room left under the 6-stage ring (schedule.cpp kRingBytes / kRingStages)
+    const int64_t ring_cap = (232448 - 1024 - 512) / 6 - 8 * (((maxw + 2 + 15) / 16) * 16) - 128;
+    if (!std::getenv("SYMM_NO_RING_CAP")) cap0 = std::max(cap0, (ring_cap / 128) * 128);
     for (int32_t t = 0; t < nt; ++t)
-      if (tile_pads[(size_t)t] > 0 && (block_size(t, tile_pads[(size_t)t]) > cap0 || std::getenv("SYMM_NO_PLACE"))) {
+      if (sort_tile[(size_t)t] && layout(t, true, tile_pads[(size_t)t], rec_pads[(size_t)t]).bytes > cap0) plan_tile(t, false);
+    for (int32_t t = 0; t < nt; ++t)
+      if (tile_pads[(size_t)t] > 0 &&
+          (layout(t, sort_tile[(size_t)t], tile_pads[(size_t)t], rec_pads[(size_t)t]).bytes > cap0 || std::getenv("SYMM_NO_PLACE"))) {
         const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1];
         for (int32_t r = r0; r < r1; ++r) vstart[(size_t)r] = S.prow_ptr[(size_t)r] - S.prow_ptr[(size_t)r0];
         tile_pads[(size_t)t] = 0;
@@ -382,24 +445,12 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t r0 = S.tile_ptr[(size_t)t], r1 = S.tile_ptr[(size_t)t + 1], T = r1 - r0;
     const int32_t S_ = (int32_t)(slot_ptr[(size_t)t + 1] - slot_ptr[(size_t)t]);
-    const int64_t nnz0 = S.prow_ptr[(size_t)r1] - S.prow_ptr[(size_t)r0];
-    const int64_t nnz = nnz0 + tile_pads[(size_t)t];  // entry slots incl. placement pads
-    int32_t nd = 0;
-    for (int32_t r = r0; r < r1; ++r)
-      for (int32_t i = S.prow_ptr[(size_t)r]; i < S.prow_ptr[(size_t)r + 1]; ++i) nd += (S.pcol[(size_t)i] == r);
-    const int64_t W = (int64_t)T + S_;
-    const int64_t o_start = (int64_t)sizeof(TileDesc);
-    int64_t o_lcol = align16(o_start + 4 * (int64_t)T);  // rseg u32[T]: start | length << 16
-    int64_t o_tidx = align16(o_lcol + 2 * nnz);
-    int64_t o_tptr = align16(o_tidx + 4 * (nnz0 - nd));
-    // lane positions sorted by work when that shortens the warps' lock-step
-    // lists enough (decided below, per tile)
     const int srt = sort_tile[(size_t)t];
-    int64_t o_sid = align16(o_tptr + 2 * (W + 1));
-    int64_t o_tgt = srt ? align16(o_sid + 2 * W) : o_sid;
-    int64_t o_val = align16(o_tgt + 4 * (int64_t)S_);
-    int64_t bytes = align16(o_val + 8 * nnz);
-    if (nnz >= 65536 || W >= 65535 || bytes >= 65536) { bad = t + 1; break; }
+    const Layout L = layout(t, srt != 0, tile_pads[(size_t)t], rec_pads[(size_t)t]);
+    const int64_t nnz = L.nnz, W = (int64_t)T + S_, bytes = L.bytes;
+    const int64_t o_lcol = L.o_lcol, o_tidx = L.o_tidx, o_tptr = L.o_tptr, o_sid = L.o_sid, o_tgt = L.o_tgt,
+                  o_val = L.o_val;
+    if (nnz >= 65536 || L.nrec >= 65536 || W >= 32767 || bytes >= 65536) { bad = t + 1; break; }
     TileDesc& D = desc[(size_t)t];
     std::memset(&D, 0, sizeof D);
     D.block_bytes = (int32_t)bytes;
@@ -449,15 +500,16 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     unsigned char* blk = blocks.data() + D.block_off;
     std::memcpy(blk, &D, sizeof(TileDesc));  // the descriptor travels with its block
     uint32_t* rseg = reinterpret_cast<uint32_t*>(blk + sizeof(TileDesc));
-    uint16_t* lcol = reinterpret_cast<uint16_t*>(blk + D.o_lcol);
-    uint32_t* tcsc = reinterpret_cast<uint32_t*>(blk + D.o_tidx);
+    // sorted tiles keep the local columns host side (their records carry them)
+    std::vector<uint16_t> lcol_host(D.sorted ? (size_t)D.nnz : 0);
+    uint16_t* lcol = D.sorted ? lcol_host.data() : reinterpret_cast<uint16_t*>(blk + D.o_lcol);
+    uint32_t* tcsc = reinterpret_cast<uint32_t*>(blk + D.o_tidx);  // sorted: the record lists
     uint16_t* tptr = reinterpret_cast<uint16_t*>(blk + D.o_tptr);
     int32_t* tgt = reinterpret_cast<int32_t*>(blk + D.o_tgt);
     double* val = reinterpret_cast<double*>(blk + D.o_val);
     const int32_t* st = slot_tgt.data() + slot_ptr[(size_t)t];
     // flush target of every spill slot (-1 = pad), bit 30 = first writer
-    for (int32_t j = 0; j < ns; ++j)
-      tgt[j] = st[j] < 0 ? st[j] : (st[j] | (slot_first[(size_t)(slot_ptr[(size_t)t] + j)] ? kTgtFirst : 0));
+    for (int32_t j = 0; j < ns; ++j) tgt[j] = st[j];
     const int32_t e0 = S.prow_ptr[(size_t)r0];
     const SpillRun* tr = runs.data() + run_ptr[(size_t)t];
     const int32_t nrt = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
@@ -482,8 +534,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     std::vector<int32_t> rst((size_t)std::max(T, 1), 0);
     for (int32_t l = 0; l < T; ++l) {
       rst[(size_t)l] = vstart[(size_t)(r0 + l)];
-      rseg[l] = (uint32_t)rst[(size_t)l] | ((uint32_t)rl[(size_t)l] << 16) |
-                (S.own_first[(size_t)(r0 + l)] ? kRsegFirst : 0u);
+      rseg[l] = (uint32_t)rst[(size_t)l] | ((uint32_t)rl[(size_t)l] << 16);
     }
     if (D.sorted) {
       uint16_t* sid = reinterpret_cast<uint16_t*>(blk + D.o_sid);
@@ -632,12 +683,30 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
             }
           }
       }
-    int32_t pos = 0;
-    for (int32_t i = 0; i < W; ++i) {
-      tptr[i] = (uint16_t)pos;
-      for (uint32_t q : lists[(size_t)slot_at[(size_t)i]]) tcsc[pos++] = q;
+    if (!D.sorted) {
+      int32_t pos = 0;
+      for (int32_t i = 0; i < W; ++i) {
+        tptr[i] = (uint16_t)pos;
+        for (uint32_t q : lists[(size_t)slot_at[(size_t)i]]) tcsc[pos++] = q;
+      }
+      tptr[W] = (uint16_t)pos;
+    } else {
+      // one record list per lane position: row part (val index | local
+      // column << 16), then transposed part (entry | local row << 16)
+      uint32_t* pseg = reinterpret_cast<uint32_t*>(blk + D.o_lcol);
+      const int32_t* pst = lane_pst.data() + lane_off[(size_t)t];
+      for (int32_t i = 0; i < W; ++i) {
+        const int32_t l = slot_at[(size_t)i];
+        int32_t q = pst[i];
+        const int32_t nrow = l < T ? rl[(size_t)l] : 0;
+        for (int32_t k = 0; k < nrow; ++k) {
+          const int32_t e = rst[(size_t)l] + k;
+          tcsc[q++] = (uint32_t)e | ((uint32_t)lcol[e] << 16);
+        }
+        for (uint32_t r : lists[(size_t)l]) tcsc[q++] = r;
+        pseg[i] = (uint32_t)pst[i] | ((uint32_t)(q - pst[i]) << 16);
+      }
     }
-    tptr[W] = (uint16_t)pos;
   }
   if (bad) return set_error(SYMM_ERR_SCHEDULE, "tiled format: a target is missing from its tile's spill list");
   // multi-rank: keep only this rank's tiles (descriptors re-based to the range)
@@ -651,6 +720,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     desc.swap(d2);
     blocks.swap(bl2);
   }
+  H.slot_first.swap(slot_first);
   H.desc.swap(desc);
   H.blocks.swap(blocks);
   H.slot_tgt.swap(slot_tgt);
@@ -681,7 +751,7 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
       (rc = upload(P, &d_slots, H.slots.data(), H.slots.size())) || (rc = upload(P, &d_runs, H.runs.data(), H.runs.size())) ||
       (rc = upload(P, &P->d_in_ptr, H.in_ptr.data(), H.in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
     return rc;
-  if (t_begin == 0 && t_end == (int32_t)S.tile_group.size()) {
+  if (t_begin == 0 && t_end == (int32_t)S.tile_group.size() && !std::getenv("SYMM_NO_K8")) {
     // K8 (single rank): tiles in id order, DAG of smaller-id writers, flush counters
     // phase-major order (phases are the tile colours: the DAG of conflicting
     // earlier-phase tiles is only n_phases deep)
@@ -693,7 +763,11 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     if (dq.empty()) dq.push_back(0);
     int32_t *d_order, *d_dp, *d_dq;
     unsigned int* d_done;
-    if ((rc = upload(P, &d_order, order.data(), order.size())) ||
+    uint8_t *d_of, *d_sf;
+    std::vector<uint8_t> of(S.own_first.begin(), S.own_first.end()), sf(H.slot_first.begin(), H.slot_first.end());
+    if (sf.empty()) sf.push_back(0);
+    if ((rc = upload(P, &d_of, of.data(), of.size())) || (rc = upload(P, &d_sf, sf.data(), sf.size())) ||
+        (rc = upload(P, &d_order, order.data(), order.size())) ||
         (rc = upload(P, &d_dp, S.dag_ptr.data(), S.dag_ptr.size())) ||
         (rc = upload(P, &d_dq, dq.data(), dq.size())) || (rc = dev_alloc(P, &d_done, (size_t)std::max(ntl, 1))))
       return rc;
@@ -701,6 +775,8 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     P->targs.dag_ptr = d_dp;
     P->targs.dag_pred = d_dq;
     P->targs.done = d_done;
+    P->targs.own_first = d_of;
+    P->targs.slot_first = d_sf;
     P->has_tiled_colored = true;
   }
   TiledArgs& A = P->targs;

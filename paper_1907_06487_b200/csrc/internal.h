@@ -136,11 +136,9 @@ struct TiledArgs {
   const int32_t* dag_ptr;         // [ntiles+1] predecessors of every tile id
   const int32_t* dag_pred;
   unsigned int* done;             // [ntiles] warps of the owning group that flushed (zeroed per run)
+  const uint8_t* own_first;       // [n] K8: the row's own tile writes it first (stores)
+  const uint8_t* slot_first;      // [spill slots] K8: this spill slot's tile writes its target first
 };
-// first-writer flags inside the tile block (K8 stores instead of adding):
-// rseg bit 31 (own row), tgt bit 30 (spill slot); K3/K4 mask them off
-constexpr uint32_t kRsegFirst = 0x80000000u;
-constexpr int32_t kTgtFirst = 0x40000000;
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions
   int32_t n;

@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int S = D.nspill;
 #pragma unroll 4
         for (int idx = lane; idx < S; idx += 32) {
-          const int g = tgt[idx] & ~kTgtFirst;  // (-1 pads stay negative)
+          const int g = tgt[idx];
 #ifdef K4_CHECK
           if (g >= A.check_n || T + idx + p >= A.window_cap) { printf("K4_CHECK loose t=%d g=%d idx=%d\n", t, g, idx); __trap(); }
 #endif
@@ -607,15 +607,14 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         int gr;
         if (l < T) {
           gr = row0 + l;
-          first = (rseg[l] & kRsegFirst) != 0;
+          first = __ldg(A.own_first + gr) != 0;
         } else {
-          const int tv = tgt[l - T];
-          gr = tv < 0 ? -1 : (tv & ~kTgtFirst);
-          first = tv >= 0 && (tv & kTgtFirst) != 0;
+          gr = tgt[l - T];
+          first = gr >= 0 && __ldg(A.slot_first + D.spill_off + (l - T)) != 0;
         }
         if (gr >= 0) __stcg(y + gr, (first || (A.debug_skip & 32)) ? acc : __ldcg(y + gr) + acc);  // (bit 5: no RMW)
       } else if (ATOMIC) {
-        const int gr = l < T ? row0 + l : (tgt[l - T] & ~kTgtFirst);
+        const int gr = l < T ? row0 + l : tgt[l - T];
 #ifdef K4_CHECK
         if (gr >= A.check_n) { printf("K4_CHECK flush t=%d l=%d gr=%d\n", t, l, gr); __trap(); }
 #endif
@@ -639,7 +638,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         double acc = 0.0;
         if (l < T && !(A.debug_skip & 1)) {
           const uint32_t sg = rseg[l];
-          const int eb = (int)(sg & 0xffffu), ee = eb + (int)((sg >> 16) & 0x7fffu);
+          const int eb = (int)(sg & 0xffffu), ee = eb + (int)(sg >> 16);
 #pragma unroll 4
           for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
         }
@@ -655,24 +654,17 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       // work-sorted: lane position i takes slot sid[i] and walks one list,
       // its row part then its transposed part (the lanes of a warp have
       // similar total lengths)
+      const uint32_t* pseg = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);  // start | len << 16
+      const uint32_t* rec = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);   // val index | x index << 16
       for (int i = gt; i < W; i += kGroupThreads) {
         const int l = sid[i];
         const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
-        int eb = 0, nr = 0;
-        if (l < T && !(A.debug_skip & 1)) {
-          const uint32_t sg = rseg[l];
-          eb = (int)(sg & 0xffffu);
-          nr = (int)((sg >> 16) & 0x7fffu);
-        }
-        const int jb = tptr[i];
-        const int nt = nr + ((A.debug_skip & 2) ? 0 : tptr[i + 1] - jb);
-        const int jo = jb - nr;  // list position u >= nr is tcsc[jo + u]
+        const uint32_t ps = pseg[i];
+        const int jb = (int)(ps & 0xffffu), nt = (A.debug_skip & 3) ? 0 : (int)(ps >> 16);
         double acc = 0.0;
 #pragma unroll 4
         for (int u = 0; u < nt; ++u) {
-          uint32_t q;
-          if (u < nr) q = (uint32_t)(eb + u) | ((uint32_t)lcol[eb + u] << 16);
-          else q = tcsc[jo + u];
+          const uint32_t q = rec[jb + u];
           acc += val[q & 0xffffu] * xs[q >> 16];
         }
         flush(l, sl, acc);

@@ -265,3 +265,19 @@ def test_rcm_levels_match_oracle(name, mk):
     assert np.max(np.abs(yp - y[inv])) <= 1e-13 * max(1.0, np.max(np.abs(y)))
     with pytest.raises(Exception):
         P.build_schedule(U, reorder=2, cone_tiles=1)
+
+
+@pytest.mark.parametrize("name,mk", GRAPHS)
+def test_first_writer_flags(name, mk):
+    """K8 (tiled_colored) stores for the first writer of a row (the writer tile
+    of the lowest phase) and adds for the others: every row has exactly one
+    first writer, among the tiles that write it (own tile or spill lists)."""
+    U = mk()
+    s = P.build_schedule(U)
+    own_first = s.table("own_first").astype(np.int64)
+    spill = s.table("spill").astype(np.int64) & 0xFFFFFFFF
+    first = (spill >> 31) & 1
+    tgt = spill & 0x7FFFFFFF
+    cnt = own_first.copy()
+    np.add.at(cnt, tgt[first == 1], 1)
+    assert np.all(cnt == 1)
