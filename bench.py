@@ -489,7 +489,7 @@ def main():
 
     extra = {}
     if a.all_variants:
-        for v in ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem", "spmv"):
+        for v in ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem", "spmv", "tiled_colored"):
             try:
                 m, l, _ = timed(v, max(50, a.steps // 4), 5)
                 extra[v] = {"ms_per_step": m, "gflops": 2.0 * nf / (m / 1e3) / 1e9,
