@@ -64,6 +64,7 @@ struct symmspmv_plan {
   FixupArgs fargs{};
   // K8 tiled_colored
   bool has_tiled_colored = false;
+  unsigned int* k8_done = nullptr;  // host copy of the counters' address (memset per run)
   // K7 recursive tree
   bool has_tree = false;
   TreeArgs tree{};
@@ -743,11 +744,10 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   TileDesc* d_desc;
   unsigned char* d_blocks;
   double* d_spill;
-  int32_t *d_targets, *d_slots;
+  int32_t* d_slots;
   SpillRun* d_runs;
   int rc;
   if ((rc = upload(P, &d_desc, H.desc.data(), H.desc.size())) || (rc = upload(P, &d_blocks, H.blocks.data(), H.blocks.size())) ||
-      (rc = upload(P, &d_targets, H.slot_tgt.data(), H.slot_tgt.size())) ||
       (rc = upload(P, &d_slots, H.slots.data(), H.slots.size())) || (rc = upload(P, &d_runs, H.runs.data(), H.runs.size())) ||
       (rc = upload(P, &P->d_in_ptr, H.in_ptr.data(), H.in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
     return rc;
@@ -771,19 +771,17 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
         (rc = upload(P, &d_dp, S.dag_ptr.data(), S.dag_ptr.size())) ||
         (rc = upload(P, &d_dq, dq.data(), dq.size())) || (rc = dev_alloc(P, &d_done, (size_t)std::max(ntl, 1))))
       return rc;
-    P->targs.order = d_order;
-    P->targs.dag_ptr = d_dp;
-    P->targs.dag_pred = d_dq;
-    P->targs.done = d_done;
-    P->targs.own_first = d_of;
-    P->targs.slot_first = d_sf;
+    K8Args k8h{d_order, d_dp, d_dq, d_done, d_of, d_sf};
+    K8Args* d_k8;
+    if ((rc = upload(P, &d_k8, &k8h, 1))) return rc;
+    P->targs.k8 = d_k8;
+    P->k8_done = d_done;
     P->has_tiled_colored = true;
   }
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
   A.ntiles = ntl;
   A.blocks = d_blocks;
-  A.targets = d_targets;
   A.slots = d_slots;
   A.runs = d_runs;
   A.spill_buf = d_spill;
@@ -1042,7 +1040,7 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     P->last_launches = 2;
   } else if (variant == SYMM_VARIANT_TILED_COLORED) {
     if (!P->has_tiled_colored) return set_error(SYMM_ERR_ARG, "variant TILED_COLORED was not uploaded by this plan");
-    cudaError_t e = cudaMemsetAsync(P->targs.done, 0, sizeof(unsigned int) * (size_t)P->targs.ntiles, st);
+    cudaError_t e = cudaMemsetAsync(P->k8_done, 0, sizeof(unsigned int) * (size_t)P->targs.ntiles, st);
     if (e != cudaSuccess) return cuda_fail(e, "tile counters");
     if ((rc = launch_tiled(P->targs, x, y, P->vec, P->tiled_grid, 2, st))) return cuda_fail((cudaError_t)rc, "k_tiled<ordered>");
     P->last_launches = 1;

@@ -116,11 +116,24 @@ struct SpillRun {                 // consecutive spill targets row .. row+len-1 
   int32_t row, wid, len, pad;
 };
 
+struct K8Args {
+  // K8 (tiled_colored, MODE 2): tiles processed in phase-major order; a tile
+  // flushes after its DAG predecessors (conflicting tiles of earlier phases)
+  const int32_t* order;           // [ntiles] processing order -> tile id
+  const int32_t* dag_ptr;         // [ntiles+1] predecessors of every tile id
+  const int32_t* dag_pred;
+  unsigned int* done;             // [ntiles] warps of the owning group that flushed (zeroed per run)
+  const uint8_t* own_first;       // [n] K8: the row's own tile writes it first (stores)
+  const uint8_t* slot_first;      // [spill slots] K8: this spill slot's tile writes its target first
+};
+
 struct TiledArgs {
   const TileDesc* tiles;          // tile id order (= BFS order)
   int32_t ntiles;
   const unsigned char* blocks;
-  const int32_t* targets;         // spill target of every spill slot of all tiles (-1 = pad)
+  const struct K8Args* k8;        // K8 (tiled_colored) tables, device memory (nullptr: none).  Kept
+                                  // out of the kernel parameters: 48 more bytes of TiledArgs made
+                                  // K3/K4 1.5-2.7% slower (measured, same tile blocks)
   const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)
   const struct SpillRun* runs;    // every spill run of every tile (tile order)
   double* spill_buf;              // K3: staged contributions to other tiles' rows
@@ -130,14 +143,6 @@ struct TiledArgs {
   unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
   int32_t debug_skip;             // diagnostics only (env SYMM_DEBUG_SKIP): skip bit0 row part,
                                   // bit1 CSC part, bit2 flush, bit3 spill-x gather (wrong results)
-  // K8 (tiled_colored, MODE 2): tiles processed in phase-major order; a tile
-  // flushes after its DAG predecessors (conflicting tiles of earlier phases)
-  const int32_t* order;           // [ntiles] processing order -> tile id
-  const int32_t* dag_ptr;         // [ntiles+1] predecessors of every tile id
-  const int32_t* dag_pred;
-  unsigned int* done;             // [ntiles] warps of the owning group that flushed (zeroed per run)
-  const uint8_t* own_first;       // [n] K8: the row's own tile writes it first (stores)
-  const uint8_t* slot_first;      // [spill slots] K8: this spill slot's tile writes its target first
 };
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions

@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       auto ld = [&](int kk, int4& d, int& T) {
         const int tt = blockIdx.x + kk * G;
         if (tt < A.ntiles) {
-          const TileDesc& D = A.tiles[ORDERED ? __ldg(A.order + tt) : tt];
+          const TileDesc& D = A.tiles[ORDERED ? __ldg(A.k8->order + tt) : tt];
           const int64_t o = D.block_off;
           d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
           T = D.nrows;
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     int k = gw;
     for (int t = blockIdx.x + gw * G; t < A.ntiles; t += kGatherWarps * G, k += kGatherWarps) {
       const int s = k % NS;
-      const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(A.order + t) : t);
+      const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(A.k8->order + t) : t);
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
       const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
       const int gruns = __ldg(&Dg->gather_runs) && !(A.debug_skip & 8);
@@ -587,11 +587,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // K8: before its first store / add, a warp waits until every DAG
     // predecessor of the tile (a conflicting tile of an earlier phase) has
     // been flushed by all the warps of its group
-    const int tile_id = ORDERED ? __ldg(A.order + t) : t;
+    const int tile_id = ORDERED ? __ldg(A.k8->order + t) : t;
     if (ORDERED && !(A.debug_skip & 16)) {  // (bit 4: diagnostics, no DAG wait)
-      const int pb = __ldg(A.dag_ptr + tile_id), pe = __ldg(A.dag_ptr + tile_id + 1);
+      const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
       for (int q = pb + lane; q < pe; q += 32) {
-        const unsigned* f = A.done + __ldg(A.dag_pred + q);
+        const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
         while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(64);
       }
       __syncwarp();
@@ -607,10 +607,10 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         int gr;
         if (l < T) {
           gr = row0 + l;
-          first = __ldg(A.own_first + gr) != 0;
+          first = __ldg(A.k8->own_first + gr) != 0;
         } else {
           gr = tgt[l - T];
-          first = gr >= 0 && __ldg(A.slot_first + D.spill_off + (l - T)) != 0;
+          first = gr >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
         }
         if (gr >= 0) __stcg(y + gr, (first || (A.debug_skip & 32)) ? acc : __ldcg(y + gr) + acc);  // (bit 5: no RMW)
       } else if (ATOMIC) {
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     if (ORDERED) {  // this warp's stores of the tile are visible: count it
       __threadfence();
       __syncwarp();
-      if (lane == 0) atomicAdd(A.done + tile_id, 1u);
+      if (lane == 0) atomicAdd(A.k8->done + tile_id, 1u);
     }
     // release stage s: each warp arrives once its reads of the stage are done
     __syncwarp();
