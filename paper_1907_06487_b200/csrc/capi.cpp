@@ -59,6 +59,7 @@ struct symmspmv_plan {
   bool has_tiled = false;
   TiledArgs targs{};
   int tiled_grid = 0;
+  int32_t tiled_nnz_cap = 0;
   int tiled_occ = 0;
   int32_t* d_in_ptr = nullptr;
   FixupArgs fargs{};
@@ -751,6 +752,9 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
       (rc = upload(P, &d_slots, H.slots.data(), H.slots.size())) || (rc = upload(P, &d_runs, H.runs.data(), H.runs.size())) ||
       (rc = upload(P, &P->d_in_ptr, H.in_ptr.data(), H.in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
     return rc;
+  K8Args k8h{};
+  k8h.slots = d_slots;
+  k8h.spill_buf = d_spill;
   if (t_begin == 0 && t_end == (int32_t)S.tile_group.size() && !std::getenv("SYMM_NO_K8")) {
     // K8 (single rank): tiles in id order, DAG of smaller-id writers, flush counters
     // phase-major order (phases are the tile colours: the DAG of conflicting
@@ -771,24 +775,29 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
         (rc = upload(P, &d_dp, S.dag_ptr.data(), S.dag_ptr.size())) ||
         (rc = upload(P, &d_dq, dq.data(), dq.size())) || (rc = dev_alloc(P, &d_done, (size_t)std::max(ntl, 1))))
       return rc;
-    K8Args k8h{d_order, d_dp, d_dq, d_done, d_of, d_sf};
-    K8Args* d_k8;
-    if ((rc = upload(P, &d_k8, &k8h, 1))) return rc;
-    P->targs.k8 = d_k8;
+    k8h.order = d_order;
+    k8h.dag_ptr = d_dp;
+    k8h.dag_pred = d_dq;
+    k8h.done = d_done;
+    k8h.own_first = d_of;
+    k8h.slot_first = d_sf;
     P->k8_done = d_done;
     P->has_tiled_colored = true;
   }
+  K8Args* d_k8;
+  if ((rc = upload(P, &d_k8, &k8h, 1))) return rc;
+  P->targs.k8 = d_k8;
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
   A.ntiles = ntl;
   A.blocks = d_blocks;
-  A.slots = d_slots;
   A.runs = d_runs;
-  A.spill_buf = d_spill;
+#if defined(K4_CHECK) || defined(K4_TRACE)
   A.check_n = n;
+#endif
   A.block_cap = H.block_cap;
   A.window_cap = H.window_cap;
-  A.nnz_cap = H.nnz_cap;
+  P->tiled_nnz_cap = H.nnz_cap;
   if (const char* dbg = std::getenv("SYMM_DEBUG_SKIP")) A.debug_skip = std::atoi(dbg);  // diagnostics only
   P->fargs = FixupArgs{n, P->d_in_ptr, d_spill};
   int stages = 0;
@@ -1457,7 +1466,13 @@ extern "C" int symmspmv_debug_trace(symmspmv_plan_t* P, const double* x, double*
   if (cudaMalloc(&d, bytes) != cudaSuccess) return set_error(SYMM_ERR_OOM, "trace buffer");
   cudaMemset(d, 0, bytes);
   TiledArgs A = P->targs;
+#ifdef K4_TRACE
   A.trace = d;
+#else
+  (void)A;
+  cudaFree(d);
+  return set_error(SYMM_ERR_UNSUPPORTED, "build with -DK4_TRACE for the tiled kernel trace");
+#endif
   int rc = launch_tiled(A, x, y, P->vec, P->tiled_grid, 0, stream);
   cudaStreamSynchronize((cudaStream_t)stream);
   cudaMemcpy(host_trace, d, bytes, cudaMemcpyDeviceToHost);
@@ -1706,7 +1721,7 @@ int symm_sweep_destroy(symm_sweep_t* W) {
 int symmspmv_plan_info(const symmspmv_plan_t* p, int32_t* out, int32_t n) {
   if (!p || !out) return set_error(SYMM_ERR_ARG, "NULL argument");
   int32_t v[8] = {p->variant, p->vec, p->tiled_grid, p->targs.stages, p->targs.block_cap, p->targs.window_cap,
-                  p->targs.nnz_cap, p->has_tiled ? tiled_smem_bytes(p->targs) : 0};
+                  p->tiled_nnz_cap, p->has_tiled ? tiled_smem_bytes(p->targs) : 0};
   int32_t m = n < 8 ? n : 8;
   for (int32_t i = 0; i < m; ++i) out[i] = v[i];
   return m;

@@ -116,7 +116,9 @@ struct SpillRun {                 // consecutive spill targets row .. row+len-1 
   int32_t row, wid, len, pad;
 };
 
-struct K8Args {
+struct K8Args {                   // (K3 / K8 tables, device memory)
+  const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)
+  double* spill_buf;              // K3: staged contributions to other tiles' rows
   // K8 (tiled_colored, MODE 2): tiles processed in phase-major order; a tile
   // flushes after its DAG predecessors (conflicting tiles of earlier phases)
   const int32_t* order;           // [ntiles] processing order -> tile id
@@ -131,18 +133,19 @@ struct TiledArgs {
   const TileDesc* tiles;          // tile id order (= BFS order)
   int32_t ntiles;
   const unsigned char* blocks;
-  const struct K8Args* k8;        // K8 (tiled_colored) tables, device memory (nullptr: none).  Kept
-                                  // out of the kernel parameters: 48 more bytes of TiledArgs made
-                                  // K3/K4 1.5-2.7% slower (measured, same tile blocks)
-  const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)
+  const struct K8Args* k8;        // K3 / K8 tables, device memory.  Kept out of the kernel
+                                  // parameters: 48 more bytes of TiledArgs made K3/K4 1.5-2.7%
+                                  // slower, 24 fewer made st27 0.6% faster (measured, same blocks)
   const struct SpillRun* runs;    // every spill run of every tile (tile order)
-  double* spill_buf;              // K3: staged contributions to other tiles' rows
-  int32_t block_cap, window_cap, nnz_cap;
+  int32_t block_cap, window_cap;
   int32_t stages;                 // smem ring depth (chosen at plan time)
-  int32_t check_n;                // K4_CHECK builds: length of the x / y vectors
-  unsigned long long* trace;      // diagnostics: per-tile event times of CTA 0 (nullptr = off)
   int32_t debug_skip;             // diagnostics only (env SYMM_DEBUG_SKIP): skip bit0 row part,
                                   // bit1 CSC part, bit2 flush, bit3 spill-x gather (wrong results)
+#if defined(K4_CHECK) || defined(K4_TRACE)
+  int32_t check_n;                // K4_CHECK builds: length of the x / y vectors
+  unsigned long long* trace;      // K4_TRACE builds: per-tile event times of CTA 0 (nullptr = off)
+#endif
+  // (kept small on purpose: every byte of kernel parameters counts, see k8)
 };
 
 struct FixupArgs {                // K3 second kernel: y[r] += sum of staged contributions

@@ -356,10 +356,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // trace layout (CTA 0 only): 8 slots per local tile k
 //   0 loader issue, 1 gather saw block, 2 gather issued, 3 consumer got x,
 //   4 pass A done, 5 pass B done, 6 group id
+#ifdef K4_TRACE
 #define TRACE(k, slot)                                                               \
   do {                                                                               \
     if (A.trace != nullptr && blockIdx.x == 0) A.trace[(size_t)(k) * 8 + (slot)] = gtimer(); \
   } while (0)
+#else
+#define TRACE(k, slot) \
+  do {                 \
+  } while (0)
+#endif
 
 __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
@@ -577,7 +583,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const uint16_t* sid = reinterpret_cast<const uint16_t*>(blk + D.o_sid);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
-    const int32_t* slot = A.slots + D.spill_off;
+    const int32_t* slot = (ATOMIC || ORDERED) ? nullptr : A.k8->slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // flush of window slot l: K4 one RED per (tile, target); K3 own rows
     // stored, spill contributions staged
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       } else if (l < T) {
         y[row0 + l] = acc;
       } else if (sl >= 0) {
-        __stcg(A.spill_buf + sl, acc);
+        __stcg(A.k8->spill_buf + sl, acc);
       }
     };
     // one thread per window slot (fixed summation order per slot ->
