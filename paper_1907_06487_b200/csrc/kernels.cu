@@ -374,6 +374,13 @@ __device__ __forceinline__ void group_sync(int g) {
 // MODE 0: K3 (own rows stored, spill staged for k_fixup), 1: K4 (fp64 RED
 // into zeroed y), 2: K8 (phase-major order, DAG-ordered store / add: no
 // atomics, no zeroing, deterministic)
+// diagnostics skip bits (env SYMM_DEBUG_SKIP) only in K4_DEBUG_SKIP builds:
+// the bit tests cost the consumer loop measurable time otherwise
+#ifdef K4_DEBUG_SKIP
+#define K4_DBG A.debug_skip
+#else
+#define K4_DBG 0
+#endif
 template <int MODE, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(A.k8->order + t) : t);
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
       const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
-      const int gruns = __ldg(&Dg->gather_runs) && !(A.debug_skip & 8);
+      const int gruns = __ldg(&Dg->gather_runs) && !(K4_DBG & 8);
       // the first batch of run records (8 per lane) is loaded before the stage
       // wait, so its latency overlaps it
       int4 R[8];
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       }
       if (lane == 0 && p == 1) cp_async8(xs, x + row0);
       if (lane == 1 && p + nfull < T) cp_async8(xs + p + nfull, x + row0 + p + nfull);
-      if (A.debug_skip & 8) {
+      if (K4_DBG & 8) {
         // diagnostics: no spill gather
       } else if (gruns) {
         // long runs: one bulk copy per run (+ <= 2 8-B edge elements)
@@ -594,7 +601,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // predecessor of the tile (a conflicting tile of an earlier phase) has
     // been flushed by all the warps of its group
     const int tile_id = ORDERED ? __ldg(A.k8->order + t) : t;
-    if (ORDERED && !(A.debug_skip & 16)) {  // (bit 4: diagnostics, no DAG wait)
+    if (ORDERED && !(K4_DBG & 16)) {  // (bit 4: diagnostics, no DAG wait)
       const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
       for (int q = pb + lane; q < pe; q += 32) {
         const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
@@ -604,7 +611,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       __threadfence();
     }
     auto flush = [&](int l, int sl, double acc) {
-      if (A.debug_skip & 4) {
+      if (K4_DBG & 4) {
         // diagnostics: no flush
       } else if (ORDERED) {
         // first writer of the target (lowest phase) stores, later ones add in
@@ -618,7 +625,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
           gr = tgt[l - T];
           first = gr >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
         }
-        if (gr >= 0) __stcg(y + gr, (first || (A.debug_skip & 32)) ? acc : __ldcg(y + gr) + acc);  // (bit 5: no RMW)
+        if (gr >= 0) __stcg(y + gr, (first || (K4_DBG & 32)) ? acc : __ldcg(y + gr) + acc);  // (bit 5: no RMW)
       } else if (ATOMIC) {
         const int gr = l < T ? row0 + l : tgt[l - T];
 #ifdef K4_CHECK
@@ -642,13 +649,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         // K3: the staging slot is fetched first so its latency overlaps the sums
         const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
         double acc = 0.0;
-        if (l < T && !(A.debug_skip & 1)) {
+        if (l < T && !(K4_DBG & 1)) {
           const uint32_t sg = rseg[l];
           const int eb = (int)(sg & 0xffffu), ee = eb + (int)(sg >> 16);
 #pragma unroll 4
           for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
         }
-        const int jb = tptr[l], je = (A.debug_skip & 2) ? jb : tptr[l + 1];
+        const int jb = tptr[l], je = (K4_DBG & 2) ? jb : tptr[l + 1];
 #pragma unroll 4
         for (int j = jb; j < je; ++j) {
           const uint32_t q = tcsc[j];
@@ -666,7 +673,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int l = sid[i];
         const int sl = (!ATOMIC && l >= T) ? __ldg(slot + (l - T)) : 0;
         const uint32_t ps = pseg[i];
-        const int jb = (int)(ps & 0xffffu), nt = (A.debug_skip & 3) ? 0 : (int)(ps >> 16);
+        const int jb = (int)(ps & 0xffffu), nt = (K4_DBG & 3) ? 0 : (int)(ps >> 16);
         double acc = 0.0;
 #pragma unroll 4
         for (int u = 0; u < nt; ++u) {

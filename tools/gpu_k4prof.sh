@@ -1,5 +1,5 @@
 #!/bin/bash
-# K4 decomposition (skip bits) + ncu of k_tiled at the default tiles; CFG picks the config, NODECOMP=1 skips the sweep
+# K4 decomposition (skip bits; needs a build with make EXTRA_NVFLAGS=-DK4_DEBUG_SKIP) + ncu of k_tiled; CFG picks the config, NODECOMP=1 skips the sweep
 mkdir -p gpurun_out; C=${CFG:-st27_128}; rm -f gpurun_out/k4_decomp_$C.txt
 if [ -z "$NODECOMP" ]; then
 for s in 0 1 2 3 4 8 15; do
