@@ -322,7 +322,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     // nvcc's unroll-by-4 of the row loop runs a row's len % 4 leftover steps
     // first, so a lane's unrolled steps start at entry start + len % 4
     // (SYMM_PLACE_PEEL=0: plain starts)
-    auto peel = [&](int32_t len) { return place_peel ? (len & 3) : 0; };
+    auto peel = [&](int32_t len) { return place_peel ? (len & (kK4Unroll - 1)) : 0; };
     for (int32_t g0 = 0; g0 < W; g0 += 32) {
       std::vector<int32_t> rem;  // lanes of this warp with a row segment
       for (int32_t i = g0; i < std::min(W, g0 + 32); ++i)
@@ -565,7 +565,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
           const int32_t l = slot_at[(size_t)i];
           if (l >= T || !place_peel) continue;
           auto& e = ent[(size_t)(i - g0)];
-          const int32_t off = uni && !peel_sorted ? 0 : std::min<int32_t>((int32_t)e.size(), (uni ? rl[(size_t)l] + cl[(size_t)l] : rl[(size_t)l]) & 3);
+          const int32_t off = uni && !peel_sorted ? 0 : std::min<int32_t>((int32_t)e.size(), (uni ? rl[(size_t)l] + cl[(size_t)l] : rl[(size_t)l]) & (uni ? 3 : kK4Unroll - 1));
           std::rotate(e.begin(), e.end() - off, e.end());
         }
       }
@@ -605,7 +605,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
         for (int32_t i = g0; i < g1; ++i) {
           const int32_t l = slot_at[(size_t)i];
           nn[i - g0] = rlen(l) + (int32_t)lists[(size_t)l].size();
-          off[i - g0] = place_peel && (!uni || peel_sorted) ? (nn[i - g0] & 3) : 0;
+          off[i - g0] = place_peel && (!uni || peel_sorted) ? (nn[i - g0] & (uni ? 3 : kK4Unroll - 1)) : 0;
           P = std::max(P, off[i - g0]);
           B4 = std::max(B4, nn[i - g0] & ~3);
         }

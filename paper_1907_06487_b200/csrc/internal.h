@@ -116,6 +116,15 @@ struct SpillRun {                 // consecutive spill targets row .. row+len-1 
   int32_t row, wid, len, pad;
 };
 
+// Unroll factor of K3/K4's per-lane row and transposed loops over unsorted
+// tiles.  nvcc runs a lane's (n % unroll) leftover steps first, and the
+// builder keys its bank placement on that (capi.cpp).  Measured (same box,
+// ms, st27 / spin / lap3d_256 / fem): unroll 4: 0.0941 / 0.2027 / 0.2590 /
+// 0.2016; unroll 2: 0.0926 / 0.2027 / 0.2584 / 0.2014; unroll 1: 0.0927 /
+// 0.2022 / 0.2554 / 0.2080; unroll 8: 0.0943 / 0.2030 / 0.2586 / 0.2081.
+// Keep the pragmas in kernels.cu in step.
+constexpr int kK4Unroll = 2;
+
 struct K8Args {                   // (K3 / K8 tables, device memory)
   const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)
   double* spill_buf;              // K3: staged contributions to other tiles' rows

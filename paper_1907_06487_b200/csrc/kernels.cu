@@ -384,6 +384,7 @@ __device__ __forceinline__ void group_sync(int g) {
 template <int MODE, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
+  static_assert(kK4Unroll == 2, "the unsorted-tile loop pragmas below must match kK4Unroll");
   constexpr bool ATOMIC = MODE == 1;
   constexpr bool ORDERED = MODE == 2;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -652,11 +653,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         if (l < T && !(K4_DBG & 1)) {
           const uint32_t sg = rseg[l];
           const int eb = (int)(sg & 0xffffu), ee = eb + (int)(sg >> 16);
-#pragma unroll 4
+#pragma unroll 2  // kK4Unroll (internal.h)
           for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
         }
         const int jb = tptr[l], je = (K4_DBG & 2) ? jb : tptr[l + 1];
-#pragma unroll 4
+#pragma unroll 2  // kK4Unroll (internal.h)
         for (int j = jb; j < je; ++j) {
           const uint32_t q = tcsc[j];
           acc += val[q & 0xffffu] * xs[q >> 16];

@@ -97,8 +97,10 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
             for g0 in range(0, W, 16):
                 idx = [i for i in range(g0, min(W, g0 + 16)) if sid[i] < T]
                 n_loop = [int(pseg[i] >> 16) if srt else int(rln[sid[i]]) for i in idx]
-                # (unsorted: row loop peels len % 4 first; sorted: record loop, leftovers last)
-                res = [(int(D["o_val"]) // 8 + int(rst[sid[i]]) + (0 if srt else nl & 3)) % 16
+                # (unsorted loops unrolled by K4_UNROLL = 2 run a lane's len % 2 leftover step
+                # first; the sorted record loop runs its blocks of 4 first, leftovers last)
+                K4_UNROLL = 2
+                res = [(int(D["o_val"]) // 8 + int(rst[sid[i]]) + (0 if srt else nl & (K4_UNROLL - 1))) % 16
                        for i, nl in zip(idx, n_loop)]
                 assert len(set(res)) == len(res)
         if srt:  # the row records give every entry's local column
