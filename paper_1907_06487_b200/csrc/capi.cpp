@@ -607,16 +607,16 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
           nn[i - g0] = rlen(l) + (int32_t)lists[(size_t)l].size();
           off[i - g0] = place_peel && (!uni || peel_sorted) ? (nn[i - g0] & (uni ? 3 : kK4Unroll - 1)) : 0;
           P = std::max(P, off[i - g0]);
-          B4 = std::max(B4, nn[i - g0] & ~3);
+          B4 = std::max(B4, nn[i - g0] & ~(kK4SortedUnroll - 1));
         }
         for (int32_t i = g0; i < g1; ++i)
-          tmax = std::max(tmax, rem_last ? B4 + (nn[i - g0] & 3) : P + nn[i - g0] - off[i - g0]);
+          tmax = std::max(tmax, rem_last ? B4 + (nn[i - g0] & (kK4SortedUnroll - 1)) : P + nn[i - g0] - off[i - g0]);
         auto idx_at = [&](int32_t i, int32_t tau) -> int32_t {
           const int32_t n = nn[i - g0];
           if (rem_last) {
-            if (tau < B4) return tau < (n & ~3) ? tau : -1;
+            if (tau < B4) return tau < (n & ~(kK4SortedUnroll - 1)) ? tau : -1;
             const int32_t t = tau - B4;
-            return t < (n & 3) ? (n & ~3) + t : -1;
+            return t < (n & (kK4SortedUnroll - 1)) ? (n & ~(kK4SortedUnroll - 1)) + t : -1;
           }
           const int32_t v = tau < P ? (tau < off[i - g0] ? tau : -1) : off[i - g0] + (tau - P);
           return v < n ? v : -1;

@@ -124,6 +124,10 @@ struct SpillRun {                 // consecutive spill targets row .. row+len-1 
 // 0.2022 / 0.2554 / 0.2080; unroll 8: 0.0943 / 0.2030 / 0.2586 / 0.2081.
 // Keep the pragmas in kernels.cu in step.
 constexpr int kK4Unroll = 2;
+// Unroll factor of the sorted tiles' record loop (blocks first, leftovers
+// last; the builder's transposed-list order follows it).  fem: unroll 4
+// 0.2004, 2 0.1991, 8 0.2002 ms.
+constexpr int kK4SortedUnroll = 2;
 
 struct K8Args {                   // (K3 / K8 tables, device memory)
   const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)

@@ -384,7 +384,7 @@ __device__ __forceinline__ void group_sync(int g) {
 template <int MODE, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
-  static_assert(kK4Unroll == 2, "the unsorted-tile loop pragmas below must match kK4Unroll");
+  static_assert(kK4Unroll == 2 && kK4SortedUnroll == 2, "the loop pragmas below must match kK4Unroll / kK4SortedUnroll");
   constexpr bool ATOMIC = MODE == 1;
   constexpr bool ORDERED = MODE == 2;
   extern __shared__ __align__(128) unsigned char sm[];
@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const uint32_t ps = pseg[i];
         const int jb = (int)(ps & 0xffffu), nt = (K4_DBG & 3) ? 0 : (int)(ps >> 16);
         double acc = 0.0;
-#pragma unroll 4
+#pragma unroll 2  // kK4SortedUnroll (internal.h)
         for (int u = 0; u < nt; ++u) {
           const uint32_t q = rec[jb + u];
           acc += val[q & 0xffffu] * xs[q >> 16];
