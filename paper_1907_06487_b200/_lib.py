@@ -4,7 +4,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsymmspmv.so")
+# SYMM_LIB: diagnostics only (A/B of library builds on the same box)
+LIB_PATH = os.environ.get("SYMM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsymmspmv.so")
 
 SYMM_ORDER_PERMUTED = 0
 SYMM_ORDER_ORIGINAL = 1

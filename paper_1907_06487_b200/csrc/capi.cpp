@@ -65,6 +65,7 @@ struct symmspmv_plan {
   FixupArgs fargs{};
   // K8 tiled_colored
   bool has_tiled_colored = false;
+  bool k4_self_zero = true;         // k_tiled<1> zeroes y itself (no k_zero launch)
   unsigned int* k8_done = nullptr;  // host copy of the counters' address (memset per run)
   // K7 recursive tree
   bool has_tree = false;
@@ -784,6 +785,16 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     P->k8_done = d_done;
     P->has_tiled_colored = true;
   }
+  unsigned long long* d_zc;
+  if ((rc = dev_alloc(P, &d_zc, 1))) return rc;
+  if (cudaError_t ze = cudaMemset(d_zc, 0, sizeof(unsigned long long))) return cuda_fail(ze, "zero counter");
+  // SYMM_K4_ZERO=0: zero y with k_zero before the launch instead (A/B diagnostics)
+  const bool self_zero = !std::getenv("SYMM_K4_ZERO") || std::atoi(std::getenv("SYMM_K4_ZERO")) != 0;
+  k8h.zero_ctr = self_zero ? d_zc : nullptr;
+  P->k4_self_zero = self_zero;
+  k8h.zero_begin = P->row_begin;
+  k8h.zero_end = P->local_end;
+  if (const char* zd = std::getenv("SYMM_ZERO_DBG")) k8h.zero_dbg = std::atoi(zd);
   K8Args* d_k8;
   if ((rc = upload(P, &d_k8, &k8h, 1))) return rc;
   P->targs.k8 = d_k8;
@@ -1042,11 +1053,18 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
   } else if (variant == SYMM_VARIANT_TILED_ATOMIC) {
     if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED_ATOMIC was not uploaded by this plan");
     // x, y cover rows [row_begin, local_end); kernels index by global row id
+    // k_tiled<1> zeroes y itself (K8Args::zero_*); a rank without tiles only zeroes
     const int64_t nloc = (int64_t)P->local_end - P->row_begin;
-    if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
+    if (P->targs.ntiles <= 0 || !P->k4_self_zero) {
+      if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
+      P->last_launches = 1;
+    }
+    if (P->targs.ntiles <= 0) {
+      return SYMM_OK;
+    }
     if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, 1, st)))
       return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
-    P->last_launches = 2;
+    P->last_launches += 1;
   } else if (variant == SYMM_VARIANT_TILED_COLORED) {
     if (!P->has_tiled_colored) return set_error(SYMM_ERR_ARG, "variant TILED_COLORED was not uploaded by this plan");
     cudaError_t e = cudaMemsetAsync(P->k8_done, 0, sizeof(unsigned int) * (size_t)P->targs.ntiles, st);

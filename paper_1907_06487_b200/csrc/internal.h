@@ -140,6 +140,11 @@ struct K8Args {                   // (K3 / K8 tables, device memory)
   unsigned int* done;             // [ntiles] warps of the owning group that flushed (zeroed per run)
   const uint8_t* own_first;       // [n] K8: the row's own tile writes it first (stores)
   const uint8_t* slot_first;      // [spill slots] K8: this spill slot's tile writes its target first
+  // K4 (MODE 1) zeroes y itself (kernels.cu k4_zero_y): monotonic launch
+  // counter, +gridDim.x per launch, never reset
+  unsigned long long* zero_ctr;   // nullptr: y is zeroed by k_zero before the launch
+  int64_t zero_begin, zero_end;   // global row ids of the local y range
+  int32_t zero_dbg;               // diagnostics (env SYMM_ZERO_DBG): bit0 no stores, bit1 no wait
 };
 
 struct TiledArgs {

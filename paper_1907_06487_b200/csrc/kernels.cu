@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -39,8 +40,20 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// fp64 reduction without a return value (RED.E.ADD.F64).  Spelled out in PTX:
+// with an acquire load elsewhere in the kernel, nvcc compiled atomicAdd's
+// unused result as ATOMG (a returning atomic), which made K4 ~15% slower.
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 template <int V>
@@ -106,12 +119,12 @@ __global__ void __launch_bounds__(256) k_atomic(CsrArgs A, const double* __restr
           sum += a * xr;  // diagonal contributes once (reading R1)
         } else {
           sum += a * __ldg(x + c);   // tmp += A[idx] * x[col[idx]]
-          atomicAdd(y + c, a * xr);  // b[col[idx]] += A[idx] * x[row]  (RED.F64)
+          red_add_f64(y + c, a * xr);  // b[col[idx]] += A[idx] * x[row]  (RED.F64)
         }
       }
     }
     sum = group_sum<V>(sum);
-    if (valid && sub == 0) atomicAdd(y + row, sum);  // b[row] += tmp
+    if (valid && sub == 0) red_add_f64(y + row, sum);  // b[row] += tmp
   }
 }
 
@@ -371,6 +384,44 @@ __device__ __forceinline__ void group_sync(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroupThreads) : "memory");
 }
 
+// K4 zeroes y itself, in a prologue run by every warp except the loader (which
+// starts filling the ring at once): the CTA stores zeros over its slice of the
+// local y range and takes a ticket from a monotonic launch counter (zero_ctr,
+// 64 bit: every launch adds exactly gridDim.x, so the tickets of one launch are
+// [m G, (m+1) G) and nothing needs resetting).  Before its first flush, every
+// consumer warp waits until the counter has reached (m+1) G: the REDs of any
+// tile may hit any CTA's slice.  The tile computations before that overlap the
+// other CTAs' zeroing.  Launches of one plan are stream-ordered (one run at a
+// time).
+constexpr int kZeroThreads = kTiledThreads - 32;
+__device__ __forceinline__ void k4_zero_y(const K8Args* z, double* y, int G, int ztid,
+                                          unsigned long long* s_target) {
+  const int64_t zb = z->zero_begin, zn = z->zero_end - zb;
+  const int64_t per = ((zn + G - 1) / G + 1) & ~int64_t(1);
+  int64_t a = zb + (int64_t)blockIdx.x * per;
+  const int64_t e = min(zb + zn, a + per);
+  if (!(z->zero_dbg & 1) && a < e) {
+    if (((uintptr_t)(y + a) & 15) && ztid == 0) y[a] = 0.0;  // 16-B stores for the aligned body
+    a += ((uintptr_t)(y + a) & 15) ? 1 : 0;
+    const int64_t nb = (e - a) / 2;
+    double2* y2 = reinterpret_cast<double2*>(y + a);
+    for (int64_t i = ztid; i < nb; i += kZeroThreads) y2[i] = make_double2(0.0, 0.0);
+    if (ztid == 0 && a + 2 * nb < e) y[e - 1] = 0.0;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kZeroThreads) : "memory");
+  if (ztid == 0) {
+    __threadfence();
+    *s_target = (z->zero_dbg & 2) ? 0ull : (atomicAdd(z->zero_ctr, 1ull) / (unsigned)G + 1) * (unsigned)G;
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kZeroThreads) : "memory");
+}
+// one poller per warp, once per launch
+__device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long t) {
+  if ((threadIdx.x & 31) == 0)
+    while (ld_acquire_u64(z->zero_ctr) < t) __nanosleep(128);
+  __syncwarp();
+}
+
 // MODE 0: K3 (own rows stored, spill staged for k_fixup), 1: K4 (fp64 RED
 // into zeroed y), 2: K8 (phase-major order, DAG-ordered store / add: no
 // atomics, no zeroing, deterministic)
@@ -403,6 +454,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     loader_k = 0;
   }
   __syncthreads();
+  __shared__ unsigned long long zero_target;
+  const bool self_zero = ATOMIC && A.k8->zero_ctr != nullptr;
+  if (self_zero && wid != kGroups * kGroupWarps) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel of the stream is done
+    k4_zero_y(A.k8, y, G, wid < kGroups * kGroupWarps ? tid : tid - 32, &zero_target);
+  }
   if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
     // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
@@ -562,9 +619,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     return;
   }
   // -------------------------------------------------- consumer groups
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // y is zeroed (PDL prerequisite done)
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel of the stream is done
   const int g = wid / kGroupWarps;
   const int gt = tid - g * kGroupThreads;
+  // K4: zero this CTA's slice of y while the loader fills the ring; the first
+  // flush of every warp waits until all CTAs have zeroed theirs (zero_ctr)
+  bool zero_pending = self_zero;
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
@@ -632,7 +692,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
 #ifdef K4_CHECK
         if (gr >= A.check_n) { printf("K4_CHECK flush t=%d l=%d gr=%d\n", t, l, gr); __trap(); }
 #endif
-        if (gr >= 0) atomicAdd(y + gr, acc);  // -1: pad slot of the spill window
+        if (gr >= 0) red_add_f64(y + gr, acc);  // -1: pad slot of the spill window
       } else if (l < T) {
         y[row0 + l] = acc;
       } else if (sl >= 0) {
@@ -643,6 +703,10 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // deterministic):
     //   own row l:  sum_{e in row l} a_e x[c_e]                    (tmp)
     //   then:       sum_{e: c_e = l, e off-diagonal} a_e x[r_e]    (b[col] += ...)
+    if (zero_pending) {  // first tile of this warp: every CTA has zeroed its slice of y
+      k4_zero_wait(A.k8, zero_target);
+      zero_pending = false;
+    }
     if (!D.sorted) {
       // slot order: a warp walks the row parts of 32 consecutive slots in
       // lock step, then their transposed parts
@@ -995,8 +1059,8 @@ CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
     if (tr) tr[2] = gtimer();
     // flush (the head's tgt list is still valid: head_empty is released below)
     if (!(A.debug_skip & 4)) {
-      for (int i = ct; i < T; i += NCT) atomicAdd(y + row0 + i, ys[i]);
-      for (int i = ct; i < S; i += NCT) atomicAdd(y + tgt[i], ys[T + i]);
+      for (int i = ct; i < T; i += NCT) red_add_f64(y + row0 + i, ys[i]);
+      for (int i = ct; i < S; i += NCT) red_add_f64(y + tgt[i], ys[T + i]);
     }
     cs_cbar(NCT);
     if (tr) tr[3] = gtimer();
@@ -1140,6 +1204,10 @@ int tiled_smem_bytes(const TiledArgs& T) {
   return T.stages * (T.block_cap + 8 * T.window_cap);
 }
 
+// The dynamic shared-memory limit is a property of the kernel, shared by every
+// plan: it is raised to the device's opt-in maximum (never lowered to one
+// plan's size, which would break launches of an earlier plan with bigger
+// blocks); each launch passes its own plan's size.
 template <int NS>
 static int tiled_attr(int smem) {
   int rc = (int)cudaFuncSetAttribute(k_tiled<0, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1159,16 +1227,30 @@ int tiled_max_ctas_per_sm(int vec, const TiledArgs& T0, int* out) {
     T.stages = ns;
     const int smem = tiled_smem_bytes(T);
     if (smem + 1024 > devsmem) continue;
+    const int lim = devsmem - 1024;  // static smem (mbarriers, loader_k) stays below 1 KB
     int rc = 0;
     switch (ns) {
-      case 8: rc = tiled_attr<8>(smem); break;
-      case 6: rc = tiled_attr<6>(smem); break;
-      case 5: rc = tiled_attr<5>(smem); break;
-      case 4: rc = tiled_attr<4>(smem); break;
-      case 3: rc = tiled_attr<3>(smem); break;
-      default: rc = tiled_attr<2>(smem); break;
+      case 8: rc = tiled_attr<8>(lim); break;
+      case 6: rc = tiled_attr<6>(lim); break;
+      case 5: rc = tiled_attr<5>(lim); break;
+      case 4: rc = tiled_attr<4>(lim); break;
+      case 3: rc = tiled_attr<3>(lim); break;
+      default: rc = tiled_attr<2>(lim); break;
     }
     if (rc) return rc;
+    // every CTA of the persistent grid (<= one per SM) must be resident at once:
+    // K4's zero wait and K8's DAG waits span CTAs
+    int occ = 0;
+    switch (ns) {
+      case 8: rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<1, 8>, kTiledThreads, smem); break;
+      case 6: rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<1, 6>, kTiledThreads, smem); break;
+      case 5: rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<1, 5>, kTiledThreads, smem); break;
+      case 4: rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<1, 4>, kTiledThreads, smem); break;
+      case 3: rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<1, 3>, kTiledThreads, smem); break;
+      default: rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<1, 2>, kTiledThreads, smem); break;
+    }
+    if (rc) return rc;
+    if (occ < 1) continue;
     *out = ns;
     return 0;
   }
@@ -1187,11 +1269,20 @@ int launch_tiled(const TiledArgs& T, const double* x, double* y, int vec, int gr
   cfg.blockDim = dim3(kTiledThreads);
   cfg.dynamicSmemBytes = (size_t)tiled_smem_bytes(T);
   cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // K4 (grid-wide zero wait) and K8 (DAG waits on other CTAs) need every CTA
+  // resident at once: a cooperative launch guarantees it or fails
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  // K8 launches cooperatively (its DAG waits span CTAs).  K4's one grid-wide wait
+  // (zeroed y) relies on the plan's grid <= SMs x occupancy (checked at plan
+  // time); a cooperative launch measured ~2.5 us slower per multiply (it gives
+  // up the overlap with the previous kernel).  SYMM_COOP=1 forces it for K4.
+  static const bool coop4 = std::getenv("SYMM_COOP") && std::atoi(std::getenv("SYMM_COOP")) != 0;
+  cfg.numAttrs = (mode == 2 || (mode == 1 && coop4)) ? 2 : 1;
   cudaError_t e = cudaErrorInvalidValue;
 #define LT(NSV)                                                                                  \
   case NSV:                                                                                      \
@@ -1224,7 +1315,7 @@ int cs_configure(CsArgs& A, int* ctas_per_sm, int nc) {
   int rc = (int)cudaErrorInvalidValue;
 #define CS_CFG(NN)                                                                                    \
   if (nc == NN) {                                                                                     \
-    rc = (int)cudaFuncSetAttribute(k_cs<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+    rc = (int)cudaFuncSetAttribute(k_cs<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, devsmem - 1024); \
     if (!rc) rc = (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k_cs<NN>, 32 * (kCsRoleWarps + NN), smem); \
   }
   CS_INSTANCES(CS_CFG)
