@@ -161,11 +161,12 @@ def _argsort_stable(vals):
     return sorted(range(len(vals)), key=lambda i: (vals[i], i))
 
 
-def alg4_balance(T_ptr, worker, level_work, kmin: int = 2, max_iter: int = 1_000_000):
+def alg4_balance(T_ptr, worker, level_work, kmin: int = 2, max_iter: int = 1_000_000, trace=None):
     """Alg. 4 "Load Balancing for two sweep, distance-2, two colors"
     (PAPER.md:2422-2494), literal loop structure; `> 2` is read as `> kmin`
     (at least k levels must remain).  Group g's color is
-    g % 2.  Returns (T_ptr, var_history)."""
+    g % 2.  Returns (T_ptr, var_history); if `trace` is a list, T_ptr at the
+    top of every outer iteration (line 17, before update) is appended to it."""
     T_ptr = list(T_ptr)
     n_g = len(T_ptr) - 1
     cum = [0]
@@ -176,6 +177,8 @@ def alg4_balance(T_ptr, worker, level_work, kmin: int = 2, max_iter: int = 1_000
     it = 0
     while not exit_ and it < max_iter:
         it += 1
+        if trace is not None:
+            trace.append(list(T_ptr))
         var, diff = _variance(T_ptr, worker, cum)
         hist.append(var)
         absRankIdx = _argsort_stable([-abs(d) for d in diff])

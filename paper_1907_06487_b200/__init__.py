@@ -178,16 +178,35 @@ class Plan:
             lib().symmspmv_destroy(self._h)
             self._h = None
 
+    def _check_dev(self, t, name):
+        """x / y must be contiguous float64 tensors on the plan's device covering
+        the plan's local rows (the kernels read / write that many elements)."""
+        if isinstance(t, int):
+            return t
+        p = _ptr(t)
+        if t.device.index != self.device:
+            raise SymmError(-1, f"{name} is on cuda:{t.device.index}, the plan on cuda:{self.device}")
+        b, e = self.local_range()
+        if t.numel() < e - b:
+            raise SymmError(-1, f"{name} has {t.numel()} elements, the plan needs {e - b}")
+        return p
+
     def run(self, x, y, stream=None, variant=None):
         """y := A x (device tensors, asynchronous on `stream`)."""
         v = -1 if variant is None else (VARIANTS[variant] if isinstance(variant, str) else int(variant))
-        check(lib().symmspmv_run_variant(self._h, v, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)),
-                                         C.c_void_p(_stream(stream))))
+        check(lib().symmspmv_run_variant(self._h, v, C.c_void_p(self._check_dev(x, "x")),
+                                         C.c_void_p(self._check_dev(y, "y")), C.c_void_p(_stream(stream))))
 
     def run_host(self, x: np.ndarray, y: np.ndarray, stream=None):
         """End to end: HOST fp64 vectors in ORIGINAL order (pinned recommended)."""
-        check(lib().symmspmv_run_host(self._h, C.c_void_p(x.ctypes.data if isinstance(x, np.ndarray) else x),
-                                      C.c_void_p(y.ctypes.data if isinstance(y, np.ndarray) else y),
+        for name, a in (("x", x), ("y", y)):
+            if not isinstance(a, np.ndarray):
+                raise TypeError(f"{name} must be a numpy array")
+            if a.dtype != np.float64 or not a.flags.c_contiguous or a.size < self.n:
+                raise SymmError(-1, f"{name} must be a C-contiguous float64 array of >= {self.n} elements")
+        if not y.flags.writeable:
+            raise SymmError(-1, "y is read-only")
+        check(lib().symmspmv_run_host(self._h, C.c_void_p(x.ctypes.data), C.c_void_p(y.ctypes.data),
                                       C.c_void_p(_stream(stream))))
 
     def local_range(self):

@@ -1666,13 +1666,27 @@ int symm_sweep_plan(const race_schedule_t* s, int32_t kind, int32_t device, symm
       ncol[(size_t)g] = std::max(ncol[(size_t)g], c + 1);
     }
   }
+  // Phases.  RACE stage-0 groups (scheme 0): groups of one parity are >= k
+  // levels apart, so the colour-c rows of all red groups
+  // form one phase, then those of the blue groups.  Any other schedule (MC /
+  // ABMC colour classes, whose groups may be adjacent; recursive-tree leaves):
+  // every (group, colour) is a phase of its own, groups in order.
+  const bool merge = S.cfg.scheme == 0;
+  std::vector<int32_t> gbase((size_t)ng + 1, 0);
   int32_t nc[2] = {0, 0};
-  for (int32_t g = 0; g < ng; ++g) nc[g & 1] = std::max(nc[g & 1], ncol[(size_t)g]);
-  auto phase_of = [&](int32_t r) { const int32_t g = gof[(size_t)r]; return (g & 1) ? nc[0] + colour[(size_t)r] : colour[(size_t)r]; };
+  for (int32_t g = 0; g < ng; ++g) {
+    nc[g & 1] = std::max(nc[g & 1], ncol[(size_t)g]);
+    gbase[(size_t)g + 1] = gbase[(size_t)g] + ncol[(size_t)g];
+  }
+  auto phase_of = [&](int32_t r) {
+    const int32_t g = gof[(size_t)r];
+    if (!merge) return gbase[(size_t)g] + colour[(size_t)r];
+    return (g & 1) ? nc[0] + colour[(size_t)r] : colour[(size_t)r];
+  };
   symm_sweep_t* W = new symm_sweep_t();
   W->kind = kind;
   W->n = n;
-  const int32_t np = nc[0] + nc[1];
+  const int32_t np = merge ? nc[0] + nc[1] : gbase[(size_t)ng];
   W->phase_ptr.assign((size_t)np + 1, 0);
   for (int32_t r = 0; r < n; ++r) W->phase_ptr[(size_t)phase_of(r) + 1]++;
   for (int32_t p = 0; p < np; ++p) W->phase_ptr[(size_t)p + 1] += W->phase_ptr[(size_t)p];

@@ -311,8 +311,9 @@ def test_tree_variant_needs_tree_schedule():
 
 
 @pytest.mark.parametrize("kind", ["gs", "kacz"])
-@pytest.mark.parametrize("name", ["lap2d_64", "st27_24", "fem_knn_30k", "lap3d_40", "spin_14"])
-def test_sweep_matches_serial_oracle(name, kind):
+@pytest.mark.parametrize("name,scheme", [("lap2d_64", 0), ("st27_24", 0), ("fem_knn_30k", 0), ("lap3d_40", 0),
+                                         ("spin_14", 0), ("st27_24", 1), ("fem_knn_30k", 2), ("lap3d_40", 3)])
+def test_sweep_matches_serial_oracle(name, scheme, kind):
     """NEXT-4: a symmetric GS / Kaczmarz sweep phase by phase on the GPU equals
     the serial oracle sweep in the plan's row order (rows of a phase commute),
     and the rows of every phase are distance-1 (GS) / distance-2 (KACZ)
@@ -323,7 +324,12 @@ def test_sweep_matches_serial_oracle(name, kind):
     U, _ = gen.make_config(name)
     if kind == "gs" and name == "spin_14":
         pytest.skip("spin diagonals in (-2, 2): Gauss-Seidel divides by near-zero pivots")
-    s = P.build_schedule(U)
+    kw = dict(scheme=scheme)
+    if scheme == 2:
+        kw["abmc_block"] = 64
+    if scheme == 3:
+        kw["n_workers"] = 296
+    s = P.build_schedule(U, **kw)
     perm, inv = s.permutation()
     sw = P.Sweep(s, kind)
     rows, ptr = sw.order()
@@ -351,3 +357,28 @@ def test_sweep_matches_serial_oracle(name, kind):
     x = xd.cpu().numpy()[perm]
     x_ref = oracle.sweep(kind, U, b, x0, inv[rows].astype(np.int32), symmetric=True)
     assert relinf(x, x_ref) <= TOL
+
+
+def test_binding_rejects_bad_vectors():
+    """The binding checks dtype, length, contiguity and device before any
+    kernel touches the memory (a short y would be written past its end)."""
+    torch = _torch()
+    import paper_1907_06487_b200 as P
+
+    U, x = gen.make_config("lap2d_64")
+    s = P.build_schedule(U)
+    plan = P.Plan(s, U, variant="tiled_atomic")
+    xd = torch.zeros(U.n, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.SymmError):
+        plan.run(xd, torch.zeros(U.n - 1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(TypeError):
+        plan.run(xd, torch.zeros(U.n, dtype=torch.float32, device="cuda"))
+    with pytest.raises(TypeError):
+        plan.run(xd, torch.zeros(2 * U.n, dtype=torch.float64, device="cuda")[::2])
+    with pytest.raises(P.SymmError):
+        plan.run_host(x, np.zeros(U.n - 1))
+    with pytest.raises(P.SymmError):
+        plan.run_host(x.astype(np.float32), np.zeros(U.n))
+    y = np.zeros(U.n)
+    plan.run_host(x, y)
+    assert relinf(y, oracle.symmspmv(U, x)) <= TOL

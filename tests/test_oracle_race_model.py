@@ -1,6 +1,7 @@
 """Pins of the RACE scheduling oracle (§4.3-§5) and the roofline model (§3)."""
 import csv
 import json
+import math
 import os
 
 import numpy as np
@@ -131,6 +132,58 @@ def test_alg4_balanced_and_blocked():
     assert T == [0, 2, 4]
 
 
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_alg4_hand_traces(case):
+    """Exact T_ptr after every outer iteration and the exact variances of a
+    hand trace of Alg. 4 (tests/golden/alg4_hand_traces.json); case 1 has
+    workers != 1, which pins reading R14's per-colour mean by value."""
+    g = _gold("alg4_hand_traces.json")
+    c = g["cases"][case]
+    trace = []
+    T, hist = race.alg4_balance(g["T_ptr0"], c["workers"], g["level_work"], kmin=2, trace=trace)
+    assert trace == c["T_trace"]
+    assert T == c["T_final"]
+    want = c.get("var_hist") or [n / d for n, d in c["var_hist_num_den"]]
+    assert len(hist) == len(want)
+    assert all(abs(h - w) <= 1e-15 * max(1.0, abs(w)) for h, w in zip(hist, want))
+
+
+def test_alg4_stencil16_ten_groups():
+    """on the 16x16 stencil with ten level groups the end
+    groups get more levels (fewer rows per level), the middle groups keep 2."""
+    g = _gold("alg4_hand_traces.json")["stencil16_ten_groups"]
+    lw, ng = g["level_sizes"], g["n_groups"]
+    L = len(lw)
+    T0 = [int(math.floor(i * L / ng + 0.5)) for i in range(ng + 1)]
+    T, hist = race.alg4_balance(T0, [1] * ng, lw, kmin=2)
+    nl = [T[i + 1] - T[i] for i in range(ng)]
+    assert T[0] == 0 and T[-1] == L and min(nl) >= 2
+    assert nl[0] > 2 and nl[-1] > 2
+    assert all(v == 2 for v in nl[2:-2])
+    # levels per group do not increase from either end toward the middle
+    assert all(nl[i] >= nl[i + 1] for i in range(ng // 2 - 1))
+    assert all(nl[-1 - i] >= nl[-2 - i] for i in range(ng // 2 - 1))
+    assert hist[-1] < hist[0]
+
+
+def test_split_window_hand_cases():
+    """Reading R13: the red part ends at the first level boundary where it holds
+    at least half the window's work, clamped so both parts keep >= k levels."""
+    lw = [1, 2, 3, 4, 5, 6]
+    # cumulative 1,3,6,10,15: 2*15 >= 21 first at boundary 5, clamped to end-k = 4
+    assert race.split_window(lw, 0, 6, 2) == 4
+    # window [2, 6): cumulative 3, 7, 12: 2*12 >= 18 first at boundary 5, clamped to end-k = 4
+    assert race.split_window(lw, 2, 6, 2) == 4
+    assert race.split_window([5, 5, 5, 5], 0, 4, 2) == 2
+    assert race.split_window([9, 1, 1, 1, 1, 1, 1, 1], 0, 8, 2) == 2  # heavy first level: clamp to first + k
+    assert race.split_window([1, 1, 1], 0, 3, 2) == 2  # < 2k levels: first + ceil(3/2)
+
+
 def test_alg4_improves_skewed_17_levels():
     """Fig. 10-like: 17 levels, 6 groups, skewed start."""
     lw = [1, 2, 3, 5, 8, 9, 10, 10, 10, 9, 8, 7, 5, 4, 3, 2, 1]
@@ -145,7 +198,8 @@ def test_nrows_eff_and_eta():
     assert race.nrows_eff([10, 6]) == 16
     assert race.nrows_eff([[10, 9, 12, 11], 5]) == 12 + 11 + 5  # inner {10,12}/{9,11} -> 23
     e = _ex()["eta_stencil16"]
-    eta = 256 / (e["nrowsEff_root"] * e["nthreads"])
+    # the 44-row tree itself is a lost figure: its root nrowsEff (printed, 44) stands for it
+    eta = race.eta(256, e["nrowsEff_root"], e["nthreads"])
     assert round(eta, 2) == e["eta"]
     assert round(eta * 8, 1) == e["speedup"]
     assert race.eta(256, [256, 0], 1) == 1.0
