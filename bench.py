@@ -3,15 +3,18 @@
 
 One "step" = one SymmSpMV y := A x (the whole hot path) over
 one synthetic matrix of a BASELINE.json config, inputs resident in HBM.
-Default workload: configs[1] (27-point stencil 128^3, randomly shuffled, then
-BFS-permuted by the schedule builder).  x and y rotate through ring buffers
-whose total size exceeds twice the L2 (PAPER.md:2045 protocol), and the
-matrix stream itself (>= 355 MB) exceeds L2 every step.
+Default workload: configs[4], the 7-point 512^3 Laplacian (the largest
+single-GPU configuration and BASELINE.md's primary one).  The same run also
+times configs[1..3] and configs[0] and reports them under `per_config`, each
+with its own roofline, cpu_baseline, e2e and sampled parity.  x and y rotate
+through ring buffers whose total size exceeds twice the L2 (PAPER.md:2045
+protocol), and the matrix stream itself exceeds L2 every step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--variant V]
     python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
 
-Prints ONE JSON line (rank 0).
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU).  Prints ONE JSON line (rank 0).
 """
 from __future__ import annotations
 
@@ -34,21 +37,26 @@ METRIC = "SymmSpMV GFLOP/s and % of HBM roofline (1/2/4/8 B200) vs host-core ora
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--config", default="st27_128")
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="lap3d_512")
+    ap.add_argument("--no-per-config", action="store_true", help="time only --config (no per_config block)")
+    ap.add_argument("--soak-ms", type=float, default=250.0,
+                    help="untimed steps right before the timed region (clock sampler running) [ms]")
     ap.add_argument("--variant", default="auto", choices=["tiled", "tiled_atomic", "atomic", "colored", "colored_smem", "spmv", "tree", "tiled_colored", "auto"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sweep", default=None, choices=["gs", "kacz"],
                     help="NEXT-4: time symmetric Gauss-Seidel / Kaczmarz sweeps instead of SymmSpMV (own JSON line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--all-variants", action="store_true", help="also time the other variants (extra key)")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--tile-nnz", type=int, default=0, help="race_config.max_tile_nnz override")
     ap.add_argument("--tile-window", type=int, default=0, help="race_config.max_tile_window override")
     ap.add_argument("--tile-work", type=int, default=0, help="race_config.tile_work override")
     ap.add_argument("--vec", type=int, default=0, help="lanes per row override")
     ap.add_argument("--sched", action="append", default=[], help="race_config override key=value (repeatable)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="multi-rank: receive the x halo before the whole run (no interior/boundary overlap)")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-rank path (row blocks + halo) even with one rank (tests the glue)")
     return ap.parse_args()
@@ -122,12 +130,20 @@ class ClockSampler:
             self._stop.set()
             self.t.join()
 
+    def mark(self):
+        """Start of the timed region (samples before it were taken during the soak)."""
+        self.mark_at = len(self.samples)
+
     def report(self):
+        m = getattr(self, "mark_at", 0)
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                     "samples": len(self.samples)}
+        timed = self.samples[m:]
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "samples_timed": len(timed), "sm_mhz_timed": statistics.median(timed) if timed else None,
+                "window": "soak (untimed steps, same kernels) + timed region"}
 
 
 def dist_env():
@@ -230,8 +246,9 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
     from paper_1907_06487_b200.dist import DistSymmSpMV
 
     t0 = time.perf_counter()
-    D = DistSymmSpMV(s, U)
+    D = DistSymmSpMV(s, U, overlap=not a.no_overlap)
     t_plan = time.perf_counter() - t0
+    parts = D.parts()
     r0, r1 = D.row_begin, D.own_end
     xp = x[inv]
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
@@ -249,7 +266,16 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
     dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, period=0.005) as clk:
+        t_s = time.perf_counter()
+        i = 0
+        while (time.perf_counter() - t_s) * 1e3 < a.soak_ms:
+            D.run(xs[i % R], ys[i % R])
+            i += 1
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark()
         ev0.record(stream)
         for i in range(a.steps):
             D.run(xs[i % R], ys[i % R])
@@ -271,6 +297,9 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
     dist.all_gather(gathered, pad)
     hb = torch.tensor([D.hx.halo_bytes()], device="cuda")
     dist.all_reduce(hb, op=dist.ReduceOp.MAX)
+    bfrac = torch.tensor([parts["boundary_nnz"] / max(1, parts["boundary_nnz"] + parts["interior_nnz"])],
+                         device="cuda", dtype=torch.float64)
+    dist.all_reduce(bfrac, op=dist.ReduceOp.MAX)
     # e2e: every step copies this rank's x slice in from pinned host memory and
     # its y rows back out (device-timed, max over ranks)
     xh = torch.from_numpy(xp[r0:r1].copy()).pin_memory()
@@ -293,6 +322,19 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
         yperm = np.concatenate([gathered[r][:int(all_sizes[r].item())].cpu().numpy() for r in range(ws)])
         y = yperm[perm]
         n = U.n
+        # parity of the timed multi-rank configuration against the full oracle,
+        # and the host-core baseline (rank 0)
+        cpu = None
+        if not a.no_cpu_baseline:
+            cb = cpu_baseline(U, x, min(3.0, a.cpu_seconds), nf, a.config)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu["cpu_model"] = cpu_model()
+            y_ref = cb["y"]
+        else:
+            import oracle
+
+            y_ref = oracle.symmspmv(U, x)
+        relerr = float(np.max(np.abs(y - y_ref)) / np.max(np.abs(y_ref)))
         bytes_min = P.min_bytes(n, int(U.nnz))
         peak, peak_src = peaks()
         achieved = bytes_min / (ms_step / 1e3) / 1e9
@@ -300,19 +342,21 @@ def run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched):
             "metric": METRIC, "value": 2.0 * nf / (ms_step / 1e3) / 1e9, "unit": "GFLOP/s", "n_gpus": ws,
             "steps": a.steps, "warmup": max(3, a.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "ours",
-            "variant": "tiled_atomic+halo", "gpu_launches": a.steps * 2 * ws,
+            "variant": "tiled_atomic+halo" + ("+overlap" if not a.no_overlap else ""),
+            "gpu_launches": a.steps * (3 if not a.no_overlap else 2) * ws,
             "config": {"workload": a.config, "n": n, "nnz_upper": int(U.nnz), "nnz_full": nf,
                        "parallelism": f"rowblock{ws}", "max_halo_bytes_per_rank": int(hb.item()),
+                       "max_boundary_nnz_frac": float(bfrac.item()),
                        "l2_policy": "inputs larger than L2 (matrix streamed once per step)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None, "bytes_per_launch": bytes_min,
                          "peak_source": peak_src + f" x {ws} GPUs"},
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
+            "parity_relinf": relerr,
             "e2e": {"value": 2.0 * nf / (float(te.item()) / 1e3) / 1e9, "unit": "GFLOP/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n, "ms_per_step": float(te.item())},
             "clocks": clk.report(),
             "schedule": {"build_s": t_sched, "plan_s": t_plan, "gen_s": t_gen},
-            "y_checksum": float(np.sum(np.abs(y))),
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
@@ -374,54 +418,76 @@ def run_sweep(a, U, x, s, nf, t_sched):
     return 0
 
 
-def main():
-    a = parse()
-    if a.impl == "reference":
-        return run_reference(a)
+PER_CONFIG = ("st27_128", "fem_knn_4M", "spin_22", "lap2d_64")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def probes(local):
+    """K5 (symm_bw_probe): load-only and copy bandwidth measured in this run."""
+    import paper_1907_06487_b200 as P
+
+    out = {}
+    for mode in ("load", "copy"):
+        try:
+            out[mode] = P.bw_probe(mode, 4 << 30, 5, device=local)
+        except Exception as e:  # noqa: BLE001
+            out[mode + "_error"] = str(e)
+    return out
+
+
+def denominators(achieved, peak, bw):
+    """Fractions of the three roofline denominators."""
+    d = {"copy_measured_peaks_json": {"gbs": peak, "frac": achieved / peak},
+         "nominal_8TBs": {"gbs": 8000.0, "frac": achieved / 8000.0}}
+    if "load" in bw:
+        d["load_only_measured_here"] = {"gbs": bw["load"], "frac": achieved / bw["load"]}
+    if "copy" in bw:
+        d["copy_measured_here"] = {"gbs": bw["copy"], "frac": achieved / bw["copy"]}
+    return d
+
+
+def bench_single(a, name, local, bw, headline, cpu_seconds):
+    """Gen + schedule + plan + timed steps of one config on this GPU; returns
+    the JSON fields of that config (the headline line or a per_config entry)."""
     import torch
 
-    ws, rank, local = dist_env()
-    if not torch.cuda.is_available():
-        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}), flush=True)
-        return 1
-    torch.cuda.set_device(local)
-    dist = None
-    if ws > 1 or a.force_dist:
-        import torch.distributed as dist
-
-        if a.force_dist and "MASTER_ADDR" not in os.environ:
-            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29531", RANK="0", WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import gen
     import paper_1907_06487_b200 as P
 
     t0 = time.perf_counter()
-    U, x = gen.make_config(a.config)
+    U, x = gen.make_config(name)
     t_gen = time.perf_counter() - t0
     nf = nnz_full_of(U)
-    t0 = time.perf_counter()
     sched_kw = {}
-    if a.tile_nnz:
-        sched_kw["max_tile_nnz"] = a.tile_nnz
-    if a.tile_window:
-        sched_kw["max_tile_window"] = a.tile_window
-        sched_kw["max_tile_rows"] = a.tile_window
-    if a.tile_work:
-        sched_kw["tile_work"] = a.tile_work
-    for kv in a.sched:
-        k_, v_ = kv.split("=")
-        sched_kw[k_] = int(v_)
+    if headline:
+        if a.tile_nnz:
+            sched_kw["max_tile_nnz"] = a.tile_nnz
+        if a.tile_window:
+            sched_kw["max_tile_window"] = a.tile_window
+            sched_kw["max_tile_rows"] = a.tile_window
+        if a.tile_work:
+            sched_kw["tile_work"] = a.tile_work
+        for kv in a.sched:
+            k_, v_ = kv.split("=")
+            sched_kw[k_] = int(v_)
+    t0 = time.perf_counter()
     s = P.build_schedule(U, **sched_kw)
     t_sched = time.perf_counter() - t0
-    if a.sweep:
-        return run_sweep(a, U, x, s, nf, t_sched)
     st = s.stats
     perm, inv = s.permutation()
-    if ws > 1 or a.force_dist:
-        return run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched)
+    all_v = headline and a.all_variants
     t0 = time.perf_counter()
-    plan = P.Plan(s, U, variant=a.variant if not a.all_variants else "auto", build_all=a.all_variants,
-                  vec_width=a.vec)
+    plan = P.Plan(s, U, variant=a.variant if not all_v else "auto", build_all=all_v, vec_width=a.vec if headline else 0)
     t_plan = time.perf_counter() - t0
     dev_bytes, bytes_min = plan.bytes()
     n = U.n
@@ -438,31 +504,33 @@ def main():
         plan.run(xs[i % R], ys[i % R], stream=stream, variant=variant)
         return plan.last_launches
 
-    def timed(variant, steps, warmup):
+    def timed(variant, steps, warmup, soak_ms):
         for i in range(warmup):
             step(i, variant)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
         torch.cuda.synchronize()
         launches = 0
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as clk:
+        with ClockSampler(local, period=0.005) as clk:
+            # soak: untimed steps so the clock record covers a loaded GPU
+            t_s = time.perf_counter()
+            i = 0
+            while soak_ms > 0 and (time.perf_counter() - t_s) * 1e3 < soak_ms:
+                for _ in range(8):
+                    step(i, variant)
+                    i += 1
+                torch.cuda.synchronize()
+            torch.cuda.synchronize()
+            clk.mark()
             ev0.record(stream)
             for i in range(steps):
                 launches += step(i, variant)
             ev1.record(stream)
             torch.cuda.synchronize()
-        ms = ev0.elapsed_time(ev1)
-        if dist:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms / steps, launches, clk.report()
+        return ev0.elapsed_time(ev1) / steps, launches, clk.report()
 
     variant = a.variant if a.variant != "auto" else "tiled_atomic"  # what AUTO runs (symmspmv.h)
-    ms_step, launches, clocks = timed(variant, a.steps, max(3, a.warmup))
+    ms_step, launches, clocks = timed(variant, a.steps, max(3, a.warmup), a.soak_ms)
 
     # per-step distribution (mean, median, min/max spread, flag > 5%),
     # from a separate pass with one event per step (not the timed number)
@@ -479,8 +547,6 @@ def main():
                   "max_ms": float(per.max()), "spread": float((per.max() - per.min()) / med),
                   "spread_over_5pct": bool((per.max() - per.min()) / med > 0.05)}
     t_s = ms_step / 1e3
-    gflops_rank = 2.0 * nf / t_s / 1e9
-    value = gflops_rank * ws  # replicas: every rank multiplies its own copy
     peak, peak_src = peaks()
     if variant == "spmv":  # the yardstick streams the full matrix (Eq. 2)
         bytes_min = spmv_min_bytes(n, nf)
@@ -488,10 +554,10 @@ def main():
     y_timed = ys[(a.steps - 1) % R].cpu().numpy()[perm]
 
     extra = {}
-    if a.all_variants:
+    if all_v:
         for v in ("atomic", "colored", "tiled", "tiled_atomic", "colored_smem", "spmv", "tiled_colored"):
             try:
-                m, l, _ = timed(v, max(50, a.steps // 4), 5)
+                m, l, _ = timed(v, max(50, a.steps // 4), 5, 0)
                 extra[v] = {"ms_per_step": m, "gflops": 2.0 * nf / (m / 1e3) / 1e9,
                             "hbm_frac": bytes_min / (m / 1e3) / 1e9 / peak, "launches_per_step": l / max(50, a.steps // 4)}
                 if v == "spmv":  # the yardstick against its own Eq. 2 bytes (alpha = 1/NNZR)
@@ -504,58 +570,145 @@ def main():
     # e2e: host buffers through the C ABI (H2D x, permute, run, unpermute, D2H y)
     xh = torch.from_numpy(x.copy()).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
-    e2e_steps = max(5, min(50, a.steps // 20))
+    e2e_steps = max(5, min(50, a.steps // 4))
     for _ in range(2):
-        plan.run_host(xh.data_ptr(), yh.data_ptr(), stream=stream)
-    if dist:
-        dist.barrier()
+        plan.run_host(xh.numpy(), yh.numpy(), stream=stream)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        plan.run_host(xh.data_ptr(), yh.data_ptr(), stream=stream)
+        plan.run_host(xh.numpy(), yh.numpy(), stream=stream)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e = {"value": 2.0 * nf / e2e_s / 1e9 * ws, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
-           "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3}
+    e2e = {"value": 2.0 * nf / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_s * 1e3,
+           "path": "symmspmv_run_host: pinned host x -> H2D, permute, run, unpermute, D2H y (wall clock)"}
+    del plan, xs, ys
 
     cpu, err = None, None
-    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+    if cpu_seconds > 0:
         # cpu_baseline leg: the oracle timed on the host, and its result compared
         # with the last timed GPU output on sampled rows
-        cb = cpu_baseline(U, x, a.cpu_seconds, nf, a.config)
+        cb = cpu_baseline(U, x, cpu_seconds, nf, name)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        cpu["openmp"] = {k: v for k, v in cpu_baseline_omp(U, x, max(2.0, a.cpu_seconds / 2), nf, a.config).items()
+        cpu["cpu_model"] = cpu_model()
+        cpu["openmp"] = {k: v for k, v in cpu_baseline_omp(U, x, max(1.0, cpu_seconds / 2), nf, name).items()
                          if k != "seconds_per_step"}
+        cpu["openmp"]["cpu_model"] = cpu["cpu_model"]
         y_ref = cb["y"]
         sample = np.random.default_rng(0).choice(n, size=min(n, 4096), replace=False)
         err = float(np.max(np.abs(y_timed[sample] - y_ref[sample])) / np.max(np.abs(y_ref)))
 
-    line = {
-        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": a.steps, "warmup": max(3, a.warmup),
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "ours", "variant": variant, "gpu_launches": launches, "step_stats": step_stats,
-        "config": {"workload": a.config, "n": n, "nnz_upper": int(U.nnz), "nnz_full": nf,
-                   "parallelism": f"replicas{ws}" if ws > 1 else "single",
+    l2_resident = 24 * n + 12 * int(U.nnz) < l2 // 2
+    out = {
+        "value": 2.0 * nf / t_s / 1e9, "ms_per_step": ms_step, "variant": variant, "gpu_launches": launches,
+        "step_stats": step_stats,
+        "config": {"workload": name, "n": n, "nnz_upper": int(U.nnz), "nnz_full": nf,
                    "l2_policy": f"inputs larger than L2: matrix {dev_bytes / 1e6:.0f} MB streamed per step; "
-                                f"x/y ring of {R} vectors each ({2 * R * 8 * n / 1e6:.0f} MB)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(a.config, variant), "bytes_per_launch": bytes_min,
-                     "peak_source": peak_src,
-                     "bytes_model": "12 nnz_u + 4 (n+1) + 24 n (Eq. 3 at alpha = 1/SymmNNZR)"},
+                                f"x/y ring of {R} vectors each ({2 * R * 8 * n / 1e6:.0f} MB)"
+                   if not l2_resident else "L2-resident working set (latency-bound config; no HBM fraction claimed)"},
+        "roofline": {"bound": "hbm" if not l2_resident else "latency (L2-resident)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(name, variant), "bytes_per_launch": bytes_min, "peak_source": peak_src,
+                     "bytes_model": "12 nnz_u + 4 (n+1) + 24 n (Eq. 3 at alpha = 1/SymmNNZR)",
+                     "denominators": denominators(achieved, peak, bw)},
         "frac_of_nominal_8TBs": achieved / 8000.0,
-        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-        "parity_sampled_relinf": err,
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "parity_sampled_relinf": err,
         "schedule": {"build_s": t_sched, "plan_s": t_plan, "gen_s": t_gen, "tiles": st["n_tiles"],
                      "phases": st["n_phases"], "levels": st["total_levels"], "eta": st["eta"],
                      "max_subcolors": st["max_subcolors"], "mean_subcolors": st["mean_subcolors"],
                      "bw_before": st["bandwidth_before"], "bw_after": st["bandwidth_after"],
-                     "spill_entries": st["spill_entries"], "device_bytes": dev_bytes, "plan": plan.info()},
+                     "spill_entries": st["spill_entries"], "device_bytes": dev_bytes},
     }
     if extra:
-        line["variants"] = extra
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+        out["variants"] = extra
+    del U, x, s
+    torch.cuda.empty_cache()
+    return out
+
+
+def relaunch_under_torchrun(a):
+    """--gpus N > 1 without a torchrun environment: re-run this command as N
+    ranks (one per GPU) under torch.distributed.run."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus} but only {have} CUDA devices"}), flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def main():
+    a = parse()
+    ws, rank, local = dist_env()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(a)
+    if ws > 1 and a.gpus not in (1, ws):
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus} but WORLD_SIZE={ws}"}), flush=True)
+        return 2
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}), flush=True)
+        return 1
+    torch.cuda.set_device(local)
+    if ws > 1 or a.force_dist:
+        import torch.distributed as dist
+
+        if a.force_dist and "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29531", RANK="0", WORLD_SIZE="1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import gen
+        import paper_1907_06487_b200 as P
+
+        t0 = time.perf_counter()
+        U, x = gen.make_config(a.config)
+        t_gen = time.perf_counter() - t0
+        nf = nnz_full_of(U)
+        t0 = time.perf_counter()
+        s = P.build_schedule(U)
+        t_sched = time.perf_counter() - t0
+        perm, inv = s.permutation()
+        return run_multi(a, U, x, s, perm, inv, nf, ws, rank, local, dist, t_gen, t_sched)
+    if a.sweep:
+        import gen
+        import paper_1907_06487_b200 as P
+
+        U, x = gen.make_config(a.config)
+        nf = nnz_full_of(U)
+        t0 = time.perf_counter()
+        s = P.build_schedule(U)
+        return run_sweep(a, U, x, s, nf, time.perf_counter() - t0)
+
+    bw = probes(local)
+    head = bench_single(a, a.config, local, bw, True, 0.0 if a.no_cpu_baseline else a.cpu_seconds)
+    peak, peak_src = peaks()
+    line = {"metric": METRIC, "value": head.pop("value"), "unit": "GFLOP/s", "n_gpus": 1, "steps": a.steps,
+            "warmup": max(3, a.warmup), "ms_per_step": head.pop("ms_per_step"), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "ours"}
+    line.update(head)
+    line["config"]["parallelism"] = "single"
+    line["bw_probe_gbs"] = bw
+    if not a.no_per_config and a.variant in ("auto", "tiled_atomic") and not a.all_variants:
+        pc = {}
+        for name in PER_CONFIG:
+            if name == a.config:
+                continue
+            try:
+                pc[name] = bench_single(a, name, local, bw, False,
+                                        0.0 if a.no_cpu_baseline else min(3.0, a.cpu_seconds))
+            except Exception as e:  # noqa: BLE001
+                pc[name] = {"error": str(e)}
+        line["per_config"] = pc
+    print(json.dumps(line), flush=True)
     return 0
 
 

@@ -227,6 +227,33 @@ int symmspmv_run(symmspmv_plan_t* p, const double* x_dev, double* y_dev, void* s
 int symmspmv_run_variant(symmspmv_plan_t* p, int32_t variant, const double* x_dev, double* y_dev,
                          void* stream);
 
+/* Halo overlap for multi-rank plans.  A rank's
+ * tiles split into INTERIOR tiles (every row they read or write is an own row,
+ * < row_end) and BOUNDARY tiles (their window reaches halo rows >= row_end).
+ *   part = SYMM_PART_INTERIOR: zero y over [row_begin, local_end) and run the
+ *          interior tiles (needs only the rank's own x);
+ *   part = SYMM_PART_BOUNDARY: run the boundary tiles (needs the x halo);
+ *          must follow the INTERIOR part on the same y (stream-ordered);
+ *   part = SYMM_PART_ALL: both (= symmspmv_run).
+ * The caller receives the x halo while the interior part runs.  Single-rank
+ * plans hold every tile as interior (BOUNDARY is a no-op).  x / y as for
+ * symmspmv_run, permuted order only; variant tiled_atomic (multi-rank plans)
+ * or the plan's variant (single rank, part ALL / INTERIOR). */
+typedef enum { SYMM_PART_ALL = 0, SYMM_PART_INTERIOR = 1, SYMM_PART_BOUNDARY = 2 } symm_part;
+int symmspmv_run_part(symmspmv_plan_t* p, int32_t part, const double* x_dev, double* y_dev, void* stream);
+/* Tile and stored-nonzero counts of the two parts (any pointer may be NULL). */
+int symmspmv_plan_parts(const symmspmv_plan_t* p, int32_t* n_interior_tiles, int32_t* n_boundary_tiles,
+                        int64_t* nnz_interior, int64_t* nnz_boundary);
+
+/* K5 bandwidth probe: the measured roofline denominators (PAPER.md:440-456:
+ * the paper measures load-only and copy bandwidth and uses both, Eq. 1).
+ * mode 0 = load-only (16-B streaming loads, result folded into a never-true
+ * store), mode 1 = copy (dst := src, bytes counted read + write).  Allocates
+ * `bytes` (mode 0) or 2 x bytes (mode 1) on `device`, runs one warm-up and
+ * `reps` timed passes on `stream` (CUDA events), frees the memory and returns
+ * the best pass in *gbps (GB/s, 1e9).  SYMM_ERR_OOM if the allocation fails. */
+int symm_bw_probe(int32_t mode, int32_t device, int64_t bytes, int32_t reps, void* stream, double* gbps);
+
 /* End-to-end convenience: x_host, y_host are HOST fp64[n] in ORIGINAL order
  * (pinned memory recommended).  H2D copy, permute, run, unpermute, D2H copy,
  * all on `stream`; returns after the stream has been synchronised. */

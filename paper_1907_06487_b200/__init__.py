@@ -16,7 +16,7 @@ import numpy as np
 from . import _lib
 from ._lib import (SYMM_ORDER_ORIGINAL, SYMM_ORDER_PERMUTED, VARIANTS, SymmError, check, lib)
 
-__all__ = ["build_schedule", "Schedule", "Plan", "Sweep", "VARIANTS", "SymmError", "min_bytes", "flops",
+__all__ = ["build_schedule", "Schedule", "Plan", "Sweep", "bw_probe", "VARIANTS", "SymmError", "min_bytes", "flops",
            "SYMM_ORDER_PERMUTED", "SYMM_ORDER_ORIGINAL", "library_path"]
 
 library_path = _lib.LIB_PATH
@@ -128,6 +128,15 @@ def halo_add(y, v, stream=None):
                                   C.c_void_p(_stream(stream))))
 
 
+def bw_probe(mode: str = "load", nbytes: int = 4 << 30, reps: int = 5, device: int = 0, stream=None) -> float:
+    """Measured HBM bandwidth in GB/s (symm_bw_probe, K5): "load" = load-only
+    stream, "copy" = read + write (the roofline denominators of PAPER.md:440-456)."""
+    g = C.c_double(0.0)
+    check(lib().symm_bw_probe({"load": 0, "copy": 1}[mode], device, int(nbytes), int(reps),
+                              C.c_void_p(_stream(stream)), C.byref(g)))
+    return g.value
+
+
 def _ptr(t):
     """Device pointer of a torch CUDA float64 tensor (or a raw int)."""
     if isinstance(t, int):
@@ -196,6 +205,23 @@ class Plan:
         v = -1 if variant is None else (VARIANTS[variant] if isinstance(variant, str) else int(variant))
         check(lib().symmspmv_run_variant(self._h, v, C.c_void_p(self._check_dev(x, "x")),
                                          C.c_void_p(self._check_dev(y, "y")), C.c_void_p(_stream(stream))))
+
+    PARTS = {"all": 0, "interior": 1, "boundary": 2}
+
+    def run_part(self, part, x, y, stream=None):
+        """Multi-rank halo overlap (symmspmv_run_part): "interior" zeroes y and
+        runs the tiles that touch only own rows, "boundary" the tiles that
+        touch halo rows (after the x halo has arrived)."""
+        pt = self.PARTS[part] if isinstance(part, str) else int(part)
+        check(lib().symmspmv_run_part(self._h, pt, C.c_void_p(self._check_dev(x, "x")),
+                                      C.c_void_p(self._check_dev(y, "y")), C.c_void_p(_stream(stream))))
+
+    def parts(self) -> dict:
+        """Tiles / stored nonzeros of the interior and boundary parts."""
+        ti, tb, ni, nb = C.c_int32(0), C.c_int32(0), C.c_int64(0), C.c_int64(0)
+        check(lib().symmspmv_plan_parts(self._h, C.byref(ti), C.byref(tb), C.byref(ni), C.byref(nb)))
+        return {"interior_tiles": ti.value, "boundary_tiles": tb.value, "interior_nnz": ni.value,
+                "boundary_nnz": nb.value}
 
     def run_host(self, x: np.ndarray, y: np.ndarray, stream=None):
         """End to end: HOST fp64 vectors in ORIGINAL order (pinned recommended)."""

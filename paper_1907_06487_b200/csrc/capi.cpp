@@ -59,6 +59,12 @@ struct symmspmv_plan {
   bool has_tiled = false;
   TiledArgs targs{};
   int tiled_grid = 0;
+  // multi-rank plans: tiles that read x or write y beyond row_end (halo rows)
+  // form a second launch, so the interior tiles can run while the x halo is in
+  // flight (symmspmv_run_part); single-rank plans keep every tile in targs
+  TiledArgs targs_b{};
+  int tiled_grid_b = 0;
+  int64_t nnz_interior = 0, nnz_boundary = 0;
   int32_t tiled_nnz_cap = 0;
   int tiled_occ = 0;
   int32_t* d_in_ptr = nullptr;
@@ -749,6 +755,25 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   int32_t* d_slots;
   SpillRun* d_runs;
   int rc;
+  // interior / boundary split (multi-rank plans only): a tile is a boundary
+  // tile if its window reaches a row >= row_end (the halo)
+  std::vector<TileDesc> dbnd;
+  if (P->nranks > 1) {
+    std::vector<TileDesc> dint;
+    for (int32_t i = 0; i < ntl; ++i) {
+      const int32_t t = t_begin + i;
+      const int64_t a = S.spill_ptr[(size_t)t], b = S.spill_ptr[(size_t)t + 1];
+      const bool bnd = b > a && (int32_t)((uint32_t)S.spill[(size_t)b - 1] & kIdxMask) >= P->row_end;
+      (bnd ? dbnd : dint).push_back(H.desc[(size_t)i]);
+      (bnd ? P->nnz_boundary : P->nnz_interior) += H.desc[(size_t)i].nnz;
+    }
+    H.desc.swap(dint);
+  } else {
+    for (const TileDesc& d : H.desc) P->nnz_interior += d.nnz;
+  }
+  const int32_t nint = (int32_t)H.desc.size(), nbnd = (int32_t)dbnd.size();
+  TileDesc* d_desc_b = nullptr;
+  if (nbnd > 0 && (rc = upload(P, &d_desc_b, dbnd.data(), dbnd.size()))) return rc;
   if ((rc = upload(P, &d_desc, H.desc.data(), H.desc.size())) || (rc = upload(P, &d_blocks, H.blocks.data(), H.blocks.size())) ||
       (rc = upload(P, &d_slots, H.slots.data(), H.slots.size())) || (rc = upload(P, &d_runs, H.runs.data(), H.runs.size())) ||
       (rc = upload(P, &P->d_in_ptr, H.in_ptr.data(), H.in_ptr.size())) || (rc = dev_alloc(P, &d_spill, (size_t)std::max<int64_t>(nsp, 1))))
@@ -785,22 +810,38 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     P->k8_done = d_done;
     P->has_tiled_colored = true;
   }
+  // K4 zeroes y in the kernel (ticketed launch counter, kernels.cu k4_zero_y)
+  // when the local y is small next to the L2: the zeros then stay in L2 and
+  // the in-kernel prologue saves the k_zero launch and its tail.  A y much
+  // larger than the L2 costs its 8n bytes of DRAM writes either way; a
+  // separate full-bandwidth k_zero launch is then cheaper than zeroing inside
+  // the kernel (lap3d_512: 2.23 vs 2.33 ms; st27_128 0.0926 vs 0.0893 ms the
+  // other way).  SYMM_K4_ZERO=0/1 forces either (A/B diagnostics).
   unsigned long long* d_zc;
   if ((rc = dev_alloc(P, &d_zc, 1))) return rc;
   if (cudaError_t ze = cudaMemset(d_zc, 0, sizeof(unsigned long long))) return cuda_fail(ze, "zero counter");
-  // SYMM_K4_ZERO=0: zero y with k_zero before the launch instead (A/B diagnostics)
-  const bool self_zero = !std::getenv("SYMM_K4_ZERO") || std::atoi(std::getenv("SYMM_K4_ZERO")) != 0;
-  k8h.zero_ctr = self_zero ? d_zc : nullptr;
-  P->k4_self_zero = self_zero;
+  {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, P->device);
+    const int64_t ybytes = 8 * ((int64_t)P->local_end - P->row_begin);
+    bool self_zero = ybytes <= (int64_t)l2 / 2;
+    if (const char* e = std::getenv("SYMM_K4_ZERO")) self_zero = std::atoi(e) != 0;
+    k8h.zero_ctr = self_zero ? d_zc : nullptr;
+    P->k4_self_zero = self_zero;
+  }
   k8h.zero_begin = P->row_begin;
   k8h.zero_end = P->local_end;
   if (const char* zd = std::getenv("SYMM_ZERO_DBG")) k8h.zero_dbg = std::atoi(zd);
   K8Args* d_k8;
   if ((rc = upload(P, &d_k8, &k8h, 1))) return rc;
+  K8Args k8b = k8h;
+  k8b.zero_ctr = nullptr;  // the boundary launch follows the interior one, which zeroed y
+  K8Args* d_k8b;
+  if ((rc = upload(P, &d_k8b, &k8b, 1))) return rc;
   P->targs.k8 = d_k8;
   TiledArgs& A = P->targs;
   A.tiles = d_desc;
-  A.ntiles = ntl;
+  A.ntiles = nint;
   A.blocks = d_blocks;
   A.runs = d_runs;
 #if defined(K4_CHECK) || defined(K4_TRACE)
@@ -820,7 +861,12 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   }
   A.stages = stages;
   P->tiled_occ = stages;
-  P->tiled_grid = std::max(1, std::min(P->sms, ntl));
+  P->tiled_grid = std::max(1, std::min(P->sms, nint));
+  P->targs_b = A;
+  P->targs_b.tiles = d_desc_b;
+  P->targs_b.ntiles = nbnd;
+  P->targs_b.k8 = d_k8b;
+  P->tiled_grid_b = std::max(1, std::min(P->sms, nbnd));
   P->has_tiled = true;
   return SYMM_OK;
 }
@@ -1021,9 +1067,13 @@ int build_tree(symmspmv_plan_t* P, const Schedule& S) {
   return SYMM_OK;
 }
 
-int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cudaStream_t st) {
+int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cudaStream_t st,
+                 int part = SYMM_PART_ALL) {
   int rc = 0;
   P->last_launches = 0;
+  if (part != SYMM_PART_ALL && variant != SYMM_VARIANT_TILED_ATOMIC &&
+      !(variant == SYMM_VARIANT_AUTO && P->nranks > 1))
+    return set_error(SYMM_ERR_ARG, "run_part needs the tiled_atomic variant");
   if (P->n == 0) return SYMM_OK;
   if (variant == SYMM_VARIANT_AUTO) variant = P->variant;
   // AUTO: the fastest measured variant (profiles/) that this plan holds
@@ -1054,17 +1104,25 @@ int run_permuted(symmspmv_plan_t* P, int variant, const double* x, double* y, cu
     if (!P->has_tiled) return set_error(SYMM_ERR_ARG, "variant TILED_ATOMIC was not uploaded by this plan");
     // x, y cover rows [row_begin, local_end); kernels index by global row id
     // k_tiled<1> zeroes y itself (K8Args::zero_*); a rank without tiles only zeroes
+    // part INTERIOR (or ALL) zeroes y and runs the interior tiles; part
+    // BOUNDARY (or ALL) runs the tiles that touch halo rows
     const int64_t nloc = (int64_t)P->local_end - P->row_begin;
-    if (P->targs.ntiles <= 0 || !P->k4_self_zero) {
-      if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
-      P->last_launches = 1;
+    if (part != SYMM_PART_BOUNDARY) {
+      if (P->targs.ntiles <= 0 || !P->k4_self_zero) {
+        if ((rc = launch_zero(y, nloc, st))) return cuda_fail((cudaError_t)rc, "zero y");
+        P->last_launches = 1;
+      }
+      if (P->targs.ntiles > 0) {
+        if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, 1, st)))
+          return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
+        P->last_launches += 1;
+      }
     }
-    if (P->targs.ntiles <= 0) {
-      return SYMM_OK;
+    if (part != SYMM_PART_INTERIOR && P->targs_b.ntiles > 0) {
+      if ((rc = launch_tiled(P->targs_b, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid_b, 1, st)))
+        return cuda_fail((cudaError_t)rc, "k_tiled<atomic> (boundary tiles)");
+      P->last_launches += 1;
     }
-    if ((rc = launch_tiled(P->targs, x - P->row_begin, y - P->row_begin, P->vec, P->tiled_grid, 1, st)))
-      return cuda_fail((cudaError_t)rc, "k_tiled<atomic>");
-    P->last_launches += 1;
   } else if (variant == SYMM_VARIANT_TILED_COLORED) {
     if (!P->has_tiled_colored) return set_error(SYMM_ERR_ARG, "variant TILED_COLORED was not uploaded by this plan");
     cudaError_t e = cudaMemsetAsync(P->k8_done, 0, sizeof(unsigned int) * (size_t)P->targs.ntiles, st);
@@ -1367,7 +1425,39 @@ int symmspmv_plan_rows(const symmspmv_plan_t* p, int32_t* b, int32_t* e) {
   return SYMM_OK;
 }
 
+static int run_variant_part(symmspmv_plan_t* P, int32_t variant, const double* x, double* y, void* stream,
+                            int32_t part);
+
 int symmspmv_run_variant(symmspmv_plan_t* P, int32_t variant, const double* x, double* y, void* stream) {
+  return run_variant_part(P, variant, x, y, stream, SYMM_PART_ALL);
+}
+
+int symmspmv_run_part(symmspmv_plan_t* P, int32_t part, const double* x, double* y, void* stream) {
+  if (part < SYMM_PART_ALL || part > SYMM_PART_BOUNDARY) return set_error(SYMM_ERR_ARG, "part %d", part);
+  if (P && P->vec_order != SYMM_ORDER_PERMUTED && part != SYMM_PART_ALL)
+    return set_error(SYMM_ERR_UNSUPPORTED, "run_part takes x/y in the permuted order");
+  if (P && P->nranks == 1) {  // every tile is interior
+    if (part == SYMM_PART_BOUNDARY) {
+      P->last_launches = 0;
+      return SYMM_OK;
+    }
+    return run_variant_part(P, -1, x, y, stream, SYMM_PART_ALL);
+  }
+  return run_variant_part(P, SYMM_VARIANT_TILED_ATOMIC, x, y, stream, part);
+}
+
+int symmspmv_plan_parts(const symmspmv_plan_t* P, int32_t* n_interior_tiles, int32_t* n_boundary_tiles,
+                        int64_t* nnz_interior, int64_t* nnz_boundary) {
+  if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
+  if (n_interior_tiles) *n_interior_tiles = P->targs.ntiles;
+  if (n_boundary_tiles) *n_boundary_tiles = P->targs_b.ntiles;
+  if (nnz_interior) *nnz_interior = P->nnz_interior;
+  if (nnz_boundary) *nnz_boundary = P->nnz_boundary;
+  return SYMM_OK;
+}
+
+static int run_variant_part(symmspmv_plan_t* P, int32_t variant, const double* x, double* y, void* stream,
+                            int32_t part) {
   if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
   if (P->n > 0 && (!x || !y)) return set_error(SYMM_ERR_ARG, "NULL vector");
   if (P->nranks > 1 && variant >= 0 && variant != SYMM_VARIANT_TILED_ATOMIC && variant != SYMM_VARIANT_AUTO)
@@ -1387,7 +1477,7 @@ int symmspmv_run_variant(symmspmv_plan_t* P, int32_t variant, const double* x, d
     int e1 = launch_gather(x, P->d_inv, P->d_xp, P->n, st);
     if (e1) rc = cuda_fail((cudaError_t)e1, "gather x");
     else {
-      rc = run_permuted(P, variant < 0 ? SYMM_VARIANT_AUTO : variant, P->d_xp, P->d_yp, st);
+      rc = run_permuted(P, variant < 0 ? SYMM_VARIANT_AUTO : variant, P->d_xp, P->d_yp, st, part);
       if (!rc) {
         int e2 = launch_gather(P->d_yp, P->d_perm, y, P->n, st);
         if (e2) rc = cuda_fail((cudaError_t)e2, "gather y");
@@ -1395,7 +1485,7 @@ int symmspmv_run_variant(symmspmv_plan_t* P, int32_t variant, const double* x, d
       }
     }
   } else {
-    rc = run_permuted(P, variant < 0 ? SYMM_VARIANT_AUTO : variant, x, y, st);
+    rc = run_permuted(P, variant < 0 ? SYMM_VARIANT_AUTO : variant, x, y, st, part);
   }
   if (cur != P->device) cudaSetDevice(cur);
   return rc;
@@ -1450,6 +1540,24 @@ int symmspmv_plan_local(const symmspmv_plan_t* p, int32_t* b, int32_t* e) {
   *b = p->row_begin;
   *e = p->local_end;
   return SYMM_OK;
+}
+
+int symm_bw_probe(int32_t mode, int32_t device, int64_t bytes, int32_t reps, void* stream, double* gbps) {
+  clear_error();
+  if (!gbps || (mode != 0 && mode != 1) || bytes < 16 || reps < 1) return set_error(SYMM_ERR_ARG, "bad argument");
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(SYMM_ERR_ARG, "device %d", device);
+  }
+  const int rc = bw_probe(mode, bytes, reps, stream, gbps);
+  cudaSetDevice(cur);
+  if (rc == (int)cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return set_error(SYMM_ERR_OOM, "bandwidth probe: cannot allocate %lld bytes", (long long)bytes);
+  }
+  return rc ? cuda_fail((cudaError_t)rc, "bandwidth probe") : SYMM_OK;
 }
 
 int symmspmv_halo_add(double* y, const double* v, int64_t n, void* stream) {

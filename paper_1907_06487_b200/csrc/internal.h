@@ -286,5 +286,6 @@ int tiled_max_ctas_per_sm(int vec, const TiledArgs& T, int* out);  // returns th
 int launch_gather(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 int launch_scatter(const double* src, const int32_t* idx, double* dst, int64_t n, void* stream);
 int launch_add(double* y, const double* v, int64_t n, void* stream);
+int bw_probe(int mode, int64_t bytes, int reps, void* stream, double* gbps);  // K5 (returns cudaError_t)
 
 }  // namespace symm

@@ -1076,6 +1076,21 @@ CsArgs A, const double* __restrict__ x, double* __restrict__ y) {
 #endif
 }
 
+// K5 bandwidth probe (load-only / copy), 16-B streaming accesses, grid-stride
+__global__ void __launch_bounds__(512) k_bw_load(const double2* __restrict__ p, int64_t n2, double* sink) {
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p + i));
+    s += v.x + v.y;
+  }
+  if (s == 1.2345e-300) *sink = s;  // never true for the probe's data: keeps the loads
+}
+__global__ void __launch_bounds__(512) k_bw_copy(const double2* __restrict__ a, double2* __restrict__ b, int64_t n2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = __ldcs(a + i);
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -1332,6 +1347,44 @@ int launch_cs(const CsArgs& A, const double* x, double* y, int grid, int nc, voi
   CS_INSTANCES(CS_LAUNCH)
 #undef CS_LAUNCH
   return (int)cudaGetLastError();
+}
+
+int bw_probe(int mode, int64_t bytes, int reps, void* stream, double* gbps) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int sms = 148;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n2 = bytes / 16;
+  double2 *a = nullptr, *b = nullptr;
+  double* sink = nullptr;
+  cudaError_t e = cudaMalloc(&a, (size_t)n2 * 16);
+  if (e == cudaSuccess && mode == 1) e = cudaMalloc(&b, (size_t)n2 * 16);
+  if (e == cudaSuccess) e = cudaMalloc(&sink, 8);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a, 0, (size_t)n2 * 16, st);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  float best = 1e30f;
+  const int grid = sms * 4;
+  for (int r = 0; e == cudaSuccess && r <= reps; ++r) {
+    cudaEventRecord(e0, st);
+    if (mode == 1) k_bw_copy<<<grid, 512, 0, st>>>(a, b, n2);
+    else k_bw_load<<<grid, 512, 0, st>>>(a, n2, sink);
+    cudaEventRecord(e1, st);
+    e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;  // pass 0 is the warm-up
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFree(a);
+  if (b) cudaFree(b);
+  if (sink) cudaFree(sink);
+  if (e != cudaSuccess) return (int)e;
+  *gbps = (double)n2 * 16.0 * (mode == 1 ? 2.0 : 1.0) / (best * 1e-3) / 1e9;
+  return 0;
 }
 
 int launch_fixup(const FixupArgs& F, double* y, void* stream) {

@@ -34,6 +34,11 @@ def _rank_rows_matrix(rp, col, val, r0, r1, n_loc):
     return gen.UpperCSR(n_loc, rp_l, (col[e0:e1] - r0).astype(np.int32), val[e0:e1].copy())
 
 
+def _host_add(dst, buf):
+    """Owner-side halo add for the CPU test (on GPUs: the C-ABI halo-add kernel)."""
+    dst.add_(buf)
+
+
 def _worker(rank, ws, port, name, kw, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -55,7 +60,7 @@ def _worker(rank, ws, port, name, kw, out):
         assert np.array_equal(x_loc.numpy(), xp[r0:he])
         Ul = _rank_rows_matrix(rp, col, val, r0, r1, he - r0)
         y_loc = torch.from_numpy(oracle.symmspmv(Ul, x_loc.numpy()))
-        hx.reduce_y(y_loc)
+        hx.reduce_y(y_loc, add=_host_add)
         y_full = oracle.symmspmv(U, x)[inv]
         err = float(np.max(np.abs(y_loc.numpy()[:r1 - r0] - y_full[r0:r1]))) / float(np.max(np.abs(y_full)))
         out[rank] = (err, r0, r1, he, hx.halo_bytes())
