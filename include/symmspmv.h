@@ -85,7 +85,9 @@ typedef struct {
                                follow BFS discovery), rows re-permuted inside the group */
   int32_t min_group_levels; /* >= k: minimum levels per level group ("at least k") */
   int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
-  uint32_t flags;           /* bit 0: within-level order = original index (experimental)    */
+  uint32_t flags;           /* bit 0: within-level order = original index (experimental);
+                               bit 1: tile phases follow the stage-0 colours (red groups' tiles,
+                               then blue, greedy; default for scheme 0 is DSatur over all tiles) */
   int32_t scheme;           /* 0 = RACE (levels, groups, tiles: the default);
                                3 = RACE with the recursive tree (§4.4.1-4.4.2):
                                    level groups with > 1 worker refined stage by stage on their
@@ -226,6 +228,16 @@ int symmspmv_halo_add(double* y_dev, const double* v_dev, int64_t n, void* strea
 int symmspmv_run(symmspmv_plan_t* p, const double* x_dev, double* y_dev, void* stream);
 int symmspmv_run_variant(symmspmv_plan_t* p, int32_t variant, const double* x_dev, double* y_dev,
                          void* stream);
+
+/* Matrix powers ("in-place matrix powers and polynomials",
+ * PAPER.md:2344-2348): Y_dev row k (k = 0 .. npow-1, row stride ldy >= n
+ * doubles) := A^(k+1) x.  x_dev, Y_dev: DEVICE fp64 in the plan's vec_order,
+ * caller-owned, x must not overlap Y (SYMM_ERR_ALIAS).  Each power is one
+ * SymmSpMV of the previous one with `variant` (< 0: the plan's), all on
+ * `stream`, asynchronous.  Single-rank plans only (SYMM_ERR_UNSUPPORTED);
+ * npow < 0 or ldy < n: SYMM_ERR_ARG; npow = 0 does nothing. */
+int symmspmv_powers(symmspmv_plan_t* p, int32_t variant, const double* x_dev, double* Y_dev, int32_t npow,
+                    int64_t ldy, void* stream);
 
 /* Halo overlap for multi-rank plans.  A rank's
  * tiles split into INTERIOR tiles (every row they read or write is an own row,

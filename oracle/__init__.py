@@ -9,6 +9,7 @@ it.
 * ``liboracle.so`` (``oracle.c``): Alg. 2 SymmSpMV, Alg. 1 SpMV, mirror,
   dense matvec, Alg. 3 BFS levels (+ island rule), brute-force distance-k and
   write-conflict checks.
+* ``matrix_powers``: A^k x, k = 1..p, by repeated Alg. 2 (NEXT-4).
 * ``race.py``: §4.4.3 epsilon level aggregation, Alg. 4 load balancing, §5
   effective row count / eta — pure Python, step by step in the paper's order.
 * ``perfmodel.py``: Eq. 1-4 and the alpha inversion of §3.3.
@@ -120,6 +121,21 @@ def spmv(rp, col, val, x) -> np.ndarray:
     y = np.empty(n, dtype=np.float64)
     _lib().oracle_spmv(n, _p(rp), _p(col), _p(val), _p(x), _p(y))
     return y
+
+
+def matrix_powers(U, x, npow: int) -> np.ndarray:
+    """Matrix powers [A x, A^2 x, ..., A^npow x] (rows of the result), by the
+    plain definition y_0 = x, y_k = A y_{k-1}, each step one Alg. 2 SymmSpMV
+    (PAPER.md:730-745).  The paper names "in-place matrix powers and
+    polynomials" as the level-based formulation's next kernels
+    (§8 Conclusion); it gives no algorithm, so the oracle
+    is the definition itself."""
+    Y = np.empty((max(int(npow), 0), U.n), dtype=np.float64)
+    y = np.ascontiguousarray(x, dtype=np.float64)
+    for k in range(int(npow)):
+        y = symmspmv(U, y)
+        Y[k] = y
+    return Y
 
 
 def sweep(kind: str, U, b, x0, order, symmetric: bool = False) -> np.ndarray:

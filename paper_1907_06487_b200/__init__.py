@@ -206,6 +206,19 @@ class Plan:
         check(lib().symmspmv_run_variant(self._h, v, C.c_void_p(self._check_dev(x, "x")),
                                          C.c_void_p(self._check_dev(y, "y")), C.c_void_p(_stream(stream))))
 
+    def powers(self, x, Y, stream=None, variant=None):
+        """Matrix powers: Y[k] := A^(k+1) x, k < Y.shape[0] (symmspmv_powers;
+        Y a contiguous float64 device tensor of shape (npow, >= n))."""
+        v = -1 if variant is None else (VARIANTS[variant] if isinstance(variant, str) else int(variant))
+        if Y.dim() != 2 or Y.shape[1] < self.n or not Y.is_contiguous():
+            raise SymmError(-1, f"Y must be a contiguous (npow, >= {self.n}) tensor")
+        px = self._check_dev(x, "x")
+        py = _ptr(Y) if Y.numel() else 0
+        if Y.numel() and Y.device.index != self.device:
+            raise SymmError(-1, f"Y is on cuda:{Y.device.index}, the plan on cuda:{self.device}")
+        check(lib().symmspmv_powers(self._h, v, C.c_void_p(px), C.c_void_p(py), int(Y.shape[0]), int(Y.shape[1]),
+                                    C.c_void_p(_stream(stream))))
+
     PARTS = {"all": 0, "interior": 1, "boundary": 2}
 
     def run_part(self, part, x, y, stream=None):

@@ -50,7 +50,7 @@ EXPORTS = [
     "race_config_default", "race_build_schedule", "race_schedule_get_stats", "race_schedule_permutation",
     "race_schedule_table", "race_schedule_permuted_matrix", "race_schedule_destroy", "race_schedule_partition",
     "symmspmv_options_default", "symmspmv_plan", "symmspmv_plan_rows", "symmspmv_plan_local", "symmspmv_halo_add", "symmspmv_run", "symmspmv_run_variant", "symmspmv_run_host",
-    "symmspmv_run_part", "symmspmv_plan_parts", "symm_bw_probe",
+    "symmspmv_run_part", "symmspmv_plan_parts", "symm_bw_probe", "symmspmv_powers",
     "symmspmv_last_launches", "symmspmv_plan_bytes", "symmspmv_plan_info", "symmspmv_destroy", "symm_status_string",
     "symm_last_error", "symm_sweep_plan", "symm_sweep_run", "symm_sweep_order", "symm_sweep_destroy",
 ]
@@ -84,6 +84,7 @@ def lib():
             "symmspmv_run_variant": ([vp, i32, vp, vp, vp], C.c_int),
             "symmspmv_run_host": ([vp, vp, vp, vp], C.c_int),
             "symmspmv_run_part": ([vp, i32, vp, vp, vp], C.c_int),
+            "symmspmv_powers": ([vp, i32, vp, vp, i32, i64, vp], C.c_int),
             "symmspmv_plan_parts": ([vp, vp, vp, vp, vp], C.c_int),
             "symm_bw_probe": ([i32, i32, i64, i32, vp, vp], C.c_int),
             "symmspmv_last_launches": ([vp], C.c_int),

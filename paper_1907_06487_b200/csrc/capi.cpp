@@ -781,7 +781,9 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
   K8Args k8h{};
   k8h.slots = d_slots;
   k8h.spill_buf = d_spill;
-  if (t_begin == 0 && t_end == (int32_t)S.tile_group.size() && !std::getenv("SYMM_NO_K8")) {
+  // (K8 holds a thread's slot sums in registers: window_cap <= kK8Slots x 224)
+  if (t_begin == 0 && t_end == (int32_t)S.tile_group.size() && !std::getenv("SYMM_NO_K8") &&
+      H.window_cap <= kK8Slots * 7 * 32) {
     // K8 (single rank): tiles in id order, DAG of smaller-id writers, flush counters
     // phase-major order (phases are the tile colours: the DAG of conflicting
     // earlier-phase tiles is only n_phases deep)
@@ -1493,6 +1495,30 @@ static int run_variant_part(symmspmv_plan_t* P, int32_t variant, const double* x
 
 int symmspmv_run(symmspmv_plan_t* P, const double* x, double* y, void* stream) {
   return symmspmv_run_variant(P, -1, x, y, stream);
+}
+
+int symmspmv_powers(symmspmv_plan_t* P, int32_t variant, const double* x, double* Y, int32_t npow, int64_t ldy,
+                    void* stream) {
+  if (!P) return set_error(SYMM_ERR_ARG, "NULL plan");
+  if (P->nranks > 1) return set_error(SYMM_ERR_UNSUPPORTED, "matrix powers are single-rank");
+  if (npow < 0 || ldy < P->n) return set_error(SYMM_ERR_ARG, "npow %d, ldy %lld (n %d)", npow, (long long)ldy, P->n);
+  if (npow == 0 || P->n == 0) {
+    P->last_launches = 0;
+    return SYMM_OK;
+  }
+  if (!x || !Y) return set_error(SYMM_ERR_ARG, "NULL vector");
+  const uintptr_t xa = (uintptr_t)x, ya = (uintptr_t)Y, xb = (uintptr_t)P->n * sizeof(double),
+                  yb = (uintptr_t)(((int64_t)npow - 1) * ldy + P->n) * sizeof(double);
+  if (xa < ya + yb && ya < xa + xb) return set_error(SYMM_ERR_ALIAS, "x overlaps Y");
+  int launches = 0;
+  for (int32_t k = 0; k < npow; ++k) {
+    // y_k = A y_{k-1}, y_0 = x (the definition; oracle.matrix_powers)
+    const double* src = k == 0 ? x : Y + (int64_t)(k - 1) * ldy;
+    if (int rc = run_variant_part(P, variant, src, Y + (int64_t)k * ldy, stream, SYMM_PART_ALL)) return rc;
+    launches += P->last_launches;
+  }
+  P->last_launches = launches;
+  return SYMM_OK;
 }
 
 int symmspmv_run_host(symmspmv_plan_t* P, const double* x_host, double* y_host, void* stream) {

@@ -128,6 +128,10 @@ constexpr int kK4Unroll = 2;
 // last; the builder's transposed-list order follows it).  fem: unroll 4
 // 0.2004, 2 0.1991, 8 0.2002 ms.
 constexpr int kK4SortedUnroll = 2;
+// K8 (tiled_colored) keeps a thread's slot sums in registers until the tile's
+// DAG predecessors have flushed: at most kK8Slots slots per thread, i.e.
+// window_cap <= kK8Slots * 224 (checked at plan time).
+constexpr int kK8Slots = 8;
 
 struct K8Args {                   // (K3 / K8 tables, device memory)
   const int32_t* slots;           // K3: staging slot of every spill slot (tile order, -1 = pad)

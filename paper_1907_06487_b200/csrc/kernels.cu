@@ -128,6 +128,75 @@ __global__ void __launch_bounds__(256) k_atomic(CsrArgs A, const double* __restr
   }
 }
 
+// Sum of v over the lanes of `peers` (a __match_any_sync set containing this
+// lane), delivered to the set's lowest lane.  Pairwise tree over the set's
+// ranks: in round k every lane adds the value of the next higher lane still in
+// the set, then the lanes of odd rank drop out (their values have been taken).
+// Every lane runs every round (the shuffles need the whole warp); all sets of
+// the warp reduce at once in ceil(log2(largest set)) rounds.
+__device__ __forceinline__ double peer_sum(unsigned peers, double v, int lane) {
+  unsigned above = peers & ~((2u << lane) - 1u);          // set members above this lane
+  unsigned rank = __popc(peers & ((1u << lane) - 1u));    // set members below it
+  while (__any_sync(0xffffffffu, above != 0)) {
+    const int nxt = __ffs(above);                          // 1-based, 0: none
+    const double t = __shfl_sync(0xffffffffu, v, nxt > 0 ? nxt - 1 : lane);
+    if (nxt > 0) v += t;
+    above &= ~__ballot_sync(0xffffffffu, rank & 1u);     // odd ranks are consumed
+    rank >>= 1;
+  }
+  return v;
+}
+
+// K1 with warp-level segmented pre-reduction (north_star: "native fp64
+// atomicAdd for the transpose updates, with warp-level segmented
+// pre-reduction").  A warp walks the nonzeros of a chunk of rows flat, 32
+// consecutive stored entries per step (coalesced col / val loads), lane i on
+// entry p = base + i of row r:
+//   b[r] += a x[c]: equal r are contiguous lanes,
+//   b[c] += a x[r], c != r: neighbouring rows share columns;
+// __match_any_sync groups the lanes of equal destination, peer_sum adds them
+// and the lowest lane of each group issues one RED.F64.
+constexpr int kK1Rows = 128;  // rows per warp chunk
+__global__ void __launch_bounds__(256) k_atomic_pr(CsrArgs A, const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r0 = warp * kK1Rows; r0 < A.n; r0 += nwarps * kK1Rows) {  // warp-uniform
+    const int r1 = (int)min((int64_t)A.n, r0 + kK1Rows);
+    const int e0 = __ldg(A.row_ptr + r0), e1 = __ldg(A.row_ptr + r1);
+    int r = (int)r0;
+    for (int base = e0; base < e1; base += 32) {
+      const int p = base + lane;
+      const bool valid = p < e1;
+      double vr = 0.0, vc = 0.0;
+      int c = -1;
+      if (valid) {
+        while (__ldg(A.row_ptr + r + 1) <= p) ++r;  // this lane's row (monotone)
+        c = ld_stream_i32(A.col + p);
+        const double a = ld_stream_f64(A.val + p);
+        const double xr = __ldg(x + r);
+        if (c == r) {
+          vr = a * xr;  // diagonal contributes once (reading R1)
+        } else {
+          vr = a * __ldg(x + c);
+          vc = a * xr;
+        }
+      }
+      // row part: key r (invalid lanes get a key no valid lane has)
+      const int kr = valid ? r : -1 - lane;
+      const unsigned mr = __match_any_sync(0xffffffffu, kr);
+      vr = peer_sum(mr, vr, lane);
+      if (valid && (mr & ((1u << lane) - 1u)) == 0) red_add_f64(y + r, vr);
+      // transposed part: key c (diagonal and invalid lanes are singletons, no RED)
+      const bool hc = valid && c != r;
+      const int kc = hc ? c : -1 - lane;
+      const unsigned mc = __match_any_sync(0xffffffffu, kc);
+      vc = peer_sum(mc, vc, lane);
+      if (hc && (mc & ((1u << lane) - 1u)) == 0) red_add_f64(y + c, vc);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K6 SpMV (yardstick)
 // Alg. 1 on the full CRS: V lanes per row stream the row's
 // (col, val) pairs with non-allocating loads, gather x through L1/L2, reduce
@@ -655,38 +724,91 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // flush of window slot l: K4 one RED per (tile, target); K3 own rows
     // stored, spill contributions staged
-    // K8: before its first store / add, a warp waits until every DAG
-    // predecessor of the tile (a conflicting tile of an earlier phase) has
-    // been flushed by all the warps of its group
-    // K8: before its first store / add, a warp waits until every DAG
-    // predecessor of the tile (a conflicting tile of an earlier phase) has
-    // been flushed by all the warps of its group
     const int tile_id = ORDERED ? __ldg(A.k8->order + t) : t;
-    if (ORDERED && !(K4_DBG & 16)) {  // (bit 4: diagnostics, no DAG wait)
-      const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
-      for (int q = pb + lane; q < pe; q += 32) {
-        const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
-        while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(64);
+    if constexpr (ORDERED) {
+      // K8: the slot sums of this thread first (registers, at most kK8Slots:
+      // the plan checks window_cap), then the wait for the tile's DAG
+      // predecessors, then the flush.  The sums of tile k overlap the flushes
+      // of its predecessors: only the flush is on the DAG's critical path.
+      double acc8[kK8Slots];
+      int l8[kK8Slots];
+#pragma unroll
+      for (int u = 0; u < kK8Slots; ++u) {
+        const int i = gt + u * kGroupThreads;
+        acc8[u] = 0.0;
+        l8[u] = -1;
+        if (i < W) {
+          double acc = 0.0;
+          if (!D.sorted) {
+            if (i < T) {
+              const uint32_t sg = rseg[i];
+              const int eb = (int)(sg & 0xffffu), ee = eb + (int)(sg >> 16);
+#pragma unroll 2
+              for (int e = eb; e < ee; ++e) acc += val[e] * xs[lcol[e]];
+            }
+            const int jb = tptr[i], je = tptr[i + 1];
+#pragma unroll 2
+            for (int j = jb; j < je; ++j) {
+              const uint32_t q = tcsc[j];
+              acc += val[q & 0xffffu] * xs[q >> 16];
+            }
+            l8[u] = i;
+          } else {
+            const uint32_t* pseg = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
+            const uint32_t* rec = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
+            const uint32_t ps = pseg[i];
+            const int jb = (int)(ps & 0xffffu), nt = (int)(ps >> 16);
+#pragma unroll 2
+            for (int v = 0; v < nt; ++v) {
+              const uint32_t q = rec[jb + v];
+              acc += val[q & 0xffffu] * xs[q >> 16];
+            }
+            l8[u] = sid[i];
+          }
+          acc8[u] = acc;
+        }
       }
-      __syncwarp();
-      __threadfence();
-    }
+      if (!(K4_DBG & 16)) {  // (bit 4: diagnostics, no DAG wait)
+        const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
+        for (int q = pb + lane; q < pe; q += 32) {
+          const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
+          while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(32);
+        }
+        __syncwarp();
+        __threadfence();
+      }
+      // flush: the first writer of a target (lowest phase) stores, later ones
+      // add in phase order (the DAG); the old values of all of this thread's
+      // targets are loaded before the first store
+      int gr8[kK8Slots];
+      double old8[kK8Slots];
+#pragma unroll
+      for (int u = 0; u < kK8Slots; ++u) {
+        const int l = l8[u];
+        gr8[u] = -1;
+        old8[u] = 0.0;
+        if (l >= 0) {
+          bool first;
+          if (l < T) {
+            gr8[u] = row0 + l;
+            first = __ldg(A.k8->own_first + row0 + l) != 0;
+          } else {
+            gr8[u] = tgt[l - T];
+            first = gr8[u] >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
+          }
+          if (gr8[u] >= 0 && !first && !(K4_DBG & 32)) old8[u] = __ldcg(y + gr8[u]);  // (bit 5: no RMW)
+          else if (gr8[u] >= 0) l8[u] = -2;  // store
+        }
+      }
+      if (!(K4_DBG & 4)) {
+#pragma unroll
+        for (int u = 0; u < kK8Slots; ++u)
+          if (gr8[u] >= 0) __stcg(y + gr8[u], l8[u] == -2 ? acc8[u] : old8[u] + acc8[u]);
+      }
+    } else {
     auto flush = [&](int l, int sl, double acc) {
       if (K4_DBG & 4) {
         // diagnostics: no flush
-      } else if (ORDERED) {
-        // first writer of the target (lowest phase) stores, later ones add in
-        // phase order (the DAG): y needs no zeroing and no atomics
-        bool first;
-        int gr;
-        if (l < T) {
-          gr = row0 + l;
-          first = __ldg(A.k8->own_first + gr) != 0;
-        } else {
-          gr = tgt[l - T];
-          first = gr >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
-        }
-        if (gr >= 0) __stcg(y + gr, (first || (K4_DBG & 32)) ? acc : __ldcg(y + gr) + acc);  // (bit 5: no RMW)
       } else if (ATOMIC) {
         const int gr = l < T ? row0 + l : tgt[l - T];
 #ifdef K4_CHECK
@@ -748,6 +870,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         flush(l, sl, acc);
       }
     }
+    }  // !ORDERED
     if (gt == 0) TRACE(k, 4);
     if (ORDERED) {  // this warp's stores of the tile are visible: count it
       __threadfence();
@@ -1125,6 +1248,20 @@ int launch_atomic(const CsrArgs& A, const double* x, double* y, int vec, int sms
   if (A.n <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int threads = 256;
+  // SYMM_K1_PREREDUCE=1: the flat kernel with __match_any_sync pre-reduction
+  // (k_atomic_pr).  Not the default: measured on B200 (st27_128, ncu,
+  // profiles/r2/k1_prereduce.md) it issues 14% fewer RED instructions but
+  // takes 0.345 ms against 0.191 ms for the V-lanes-per-row kernel below,
+  // whose shuffle reduction of each row's sum is the warp-level segmented
+  // pre-reduction that pays (rows are the segments; equal transposed targets
+  // inside one warp step are rare in a bandwidth-reduced order).
+  static const bool prered = std::getenv("SYMM_K1_PREREDUCE") && std::atoi(std::getenv("SYMM_K1_PREREDUCE")) != 0;
+  if (prered) {
+    const int64_t chunks = ((int64_t)A.n + kK1Rows - 1) / kK1Rows;
+    const int64_t g = (chunks * 32 + threads - 1) / threads, gmax = (int64_t)sms * 8;
+    k_atomic_pr<<<(int)std::max<int64_t>(1, std::min(g, gmax)), threads, 0, st>>>(A, x, y);
+    return (int)cudaGetLastError();
+  }
   int64_t warps_needed = ((int64_t)A.n * vec + 31) / 32;
   int64_t g = (warps_needed * 32 + threads - 1) / threads;
   int64_t gmax = (int64_t)sms * 8;

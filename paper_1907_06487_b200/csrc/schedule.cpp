@@ -20,6 +20,7 @@
 #include <cstring>
 #include <numeric>
 #include <queue>
+#include <tuple>
 #include <omp.h>
 
 #include "internal.h"
@@ -1042,10 +1043,53 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
       std::sort(v.begin(), v.end());
     }
   }
-  // tile coloring inside each stage-0 color (greedy, ascending tile id)
+  // tile coloring.  Any proper colouring of the tile conflict graph makes
+  // every phase write-disjoint; the phase count is the
+  // depth of the colored variants' dependency chain (K2: one launch per
+  // phase; K8: the DAG's longest path).
+  //  - scheme 0 (default): DSatur over all tiles at once (reading R34):
+  //    st27_128 14 phases, fem_knn_4M 18, against 31 / 43 below;
+  //  - flags bit 1, and schemes 1-3: the stage-0 structure, every red
+  //    group's tiles before every blue group's, greedy in ascending tile id
+  //    inside each stage-0 colour.
   std::vector<int32_t> tcol((size_t)ntiles, -1);
   int32_t ncol[2] = {0, 0};
-  for (int32_t t = 0; t < ntiles; ++t) {
+  const bool dsatur = cfg.scheme == 0 && !(cfg.flags & 2u);
+  if (dsatur) {
+    // Brelaz: colour next the uncoloured tile with the most distinct colours
+    // among its neighbours (ties: more neighbours, then the smaller id), with
+    // the smallest colour none of them has
+    std::vector<std::vector<uint64_t>> sat((size_t)ntiles);
+    std::vector<int32_t> nsat((size_t)ntiles, 0);
+    using Key = std::tuple<int32_t, int32_t, int32_t>;  // (saturation, degree, -id)
+    std::priority_queue<Key> pq;
+    for (int32_t t = 0; t < ntiles; ++t) pq.emplace(0, (int32_t)conf[(size_t)t].size(), -t);
+    auto has = [&](int32_t u, int32_t c) {
+      const auto& w = sat[(size_t)u];
+      return (size_t)(c >> 6) < w.size() && ((w[(size_t)(c >> 6)] >> (c & 63)) & 1u);
+    };
+    int32_t nc = 0;
+    while (!pq.empty()) {
+      const auto [sv, dv, mt] = pq.top();
+      pq.pop();
+      const int32_t t = -mt;
+      if (tcol[(size_t)t] >= 0 || sv != nsat[(size_t)t]) continue;  // stale entry
+      int32_t c = 0;
+      while (has(t, c)) ++c;
+      tcol[(size_t)t] = c;
+      nc = std::max(nc, c + 1);
+      for (int32_t u : conf[(size_t)t]) {
+        if (tcol[(size_t)u] >= 0 || has(u, c)) continue;
+        auto& w = sat[(size_t)u];
+        if (w.size() <= (size_t)(c >> 6)) w.resize((size_t)(c >> 6) + 1, 0);
+        w[(size_t)(c >> 6)] |= uint64_t(1) << (c & 63);
+        pq.emplace(++nsat[(size_t)u], (int32_t)conf[(size_t)u].size(), -u);
+      }
+    }
+    { std::vector<std::vector<uint64_t>>().swap(sat); }
+    ncol[0] = nc;
+  }
+  for (int32_t t = 0; t < ntiles && !dsatur; ++t) {
     int32_t s0 = S->tile_group[(size_t)t] % 2;
     std::vector<char> used;
     for (int32_t u : conf[(size_t)t]) {
@@ -1061,7 +1105,7 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
   }
   S->tile_phase.assign((size_t)ntiles, 0);
   for (int32_t t = 0; t < ntiles; ++t)
-    S->tile_phase[(size_t)t] = (S->tile_group[(size_t)t] % 2 == 0) ? tcol[(size_t)t] : ncol[0] + tcol[(size_t)t];
+    S->tile_phase[(size_t)t] = (dsatur || S->tile_group[(size_t)t] % 2 == 0) ? tcol[(size_t)t] : ncol[0] + tcol[(size_t)t];
   S->n_phases = ncol[0] + ncol[1];
   // DAG: u waits for every conflicting tile of an earlier phase
   S->dag_ptr.assign((size_t)ntiles + 1, 0);

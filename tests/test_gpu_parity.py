@@ -451,3 +451,66 @@ def test_dist_symmspmv_run_gloo_one_gpu(ws, name, overlap):
     for r in range(ws):
         err, parts = out[r]
         assert err <= TOL, (r, err, parts)
+
+
+# ------------------------------------------------------------------ matrix powers (NEXT-4)
+def _powers_gpu(U, x, npow, variant, ld_pad=0, build_all=False):
+    torch = _torch()
+    import paper_1907_06487_b200 as P
+
+    s = P.build_schedule(U)
+    plan = P.Plan(s, U, variant=variant, build_all=build_all)
+    perm, inv = s.permutation()
+    xd = torch.from_numpy(x[inv].copy()).cuda()
+    Y = torch.full((npow, U.n + ld_pad), float("nan"), dtype=torch.float64, device="cuda")
+    plan.powers(xd, Y)
+    torch.cuda.synchronize()
+    return Y[:, :U.n].cpu().numpy()[:, perm], plan, xd, Y
+
+
+@pytest.mark.parametrize("variant", ["tiled_atomic", "tiled", "tiled_colored", "colored", "atomic"])
+@pytest.mark.parametrize("name", SMALL)
+def test_matrix_powers_match_oracle(name, variant):
+    """Y[k] = A^(k+1) x through symmspmv_powers vs oracle.matrix_powers, every
+    power within 1e-12 (relative inf-norm), rows padded (ldy > n)."""
+    U, x = gen.make_config(name)
+    ref = oracle.matrix_powers(U, x, 4)
+    Y, _, _, _ = _powers_gpu(U, x, 4, variant, ld_pad=5)
+    for k in range(4):
+        assert relinf(Y[k], ref[k]) <= TOL, (k, relinf(Y[k], ref[k]))
+
+
+def test_matrix_powers_full_size_and_determinism():
+    """Config 2 at full size, 3 powers with the bench variant; the deterministic
+    K8 variant gives bitwise identical powers over repeats."""
+    torch = _torch()
+    U, x = gen.make_config("st27_128")
+    ref = oracle.matrix_powers(U, x, 3)
+    Y, plan, xd, Yd = _powers_gpu(U, x, 3, "auto", build_all=True)
+    for k in range(3):
+        assert relinf(Y[k], ref[k]) <= TOL, k
+    plan.powers(xd, Yd, variant="tiled_colored")
+    torch.cuda.synchronize()
+    first = Yd.cpu().numpy()
+    for _ in range(3):
+        Yd.fill_(float("nan"))
+        plan.powers(xd, Yd, variant="tiled_colored")
+        torch.cuda.synchronize()
+        assert np.array_equal(Yd.cpu().numpy(), first)
+
+
+def test_matrix_powers_errors():
+    torch = _torch()
+    import paper_1907_06487_b200 as P
+
+    U, x = gen.make_config("lap2d_64")
+    s = P.build_schedule(U)
+    plan = P.Plan(s, U)
+    xd = torch.zeros(U.n, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.SymmError):
+        plan.powers(xd, torch.zeros((2, U.n - 1), dtype=torch.float64, device="cuda"))  # ldy < n
+    Y = torch.zeros((2, U.n), dtype=torch.float64, device="cuda")
+    with pytest.raises(P.SymmError) as e:
+        plan.powers(Y[1], Y)  # x inside Y
+    assert e.value.code == -9
+    plan.powers(xd, torch.zeros((0, U.n), dtype=torch.float64, device="cuda"))  # npow = 0: no-op

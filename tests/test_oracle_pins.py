@@ -337,3 +337,53 @@ def test_kacz_projects_onto_the_row():
         assert abs(A[i] @ x - b[i]) <= 1e-13 * (np.abs(A[i]) @ np.abs(x) + abs(b[i]))
         d = x - x0
         assert np.allclose(d, (d @ A[i]) / (A[i] @ A[i]) * A[i], atol=1e-14)
+
+
+# --------------------------------------------------------------- matrix powers (NEXT-4)
+@pytest.mark.parametrize("mk", SMALL[:6])
+def test_matrix_powers_vs_dense_matrix_power(mk):
+    """A^k x for k = 1..4 against numpy's matrix_power of the scipy-built dense
+    A = U + U^T - diag(U) (library routines, independent of the oracle)."""
+    U = mk()
+    A = scipy_full(U).toarray()
+    x = np.random.default_rng(7).uniform(-1, 1, U.n)
+    Y = oracle.matrix_powers(U, x, 4)
+    assert Y.shape == (4, U.n)
+    for k in range(1, 5):
+        ref = np.linalg.matrix_power(A, k) @ x
+        scale = np.max(np.linalg.matrix_power(np.abs(A), k) @ np.abs(x))
+        assert np.max(np.abs(Y[k - 1] - ref)) <= 1e-13 * scale, k
+
+
+@pytest.mark.parametrize("p,q", [(3, 5), (30, 28)])
+def test_matrix_powers_laplacian_modes(p, q):
+    """2-D 5-pt Laplacian on N x N: x_ij = sin(p pi i/(N+1)) sin(q pi j/(N+1)) is an
+    eigenvector, lambda = 4 - 2 cos(p pi/(N+1)) - 2 cos(q pi/(N+1)), so A^k x =
+    lambda^k x (closed form; a low and a high mode).  Bound: x's own entries
+    carry ~2u rounding (two sines and a product), amplified per step by
+    ||A - lambda I||_inf <= 8 + |lambda|, plus each product's rounding:
+    32 k u (8 + |lambda|)^k ||x||_inf."""
+    N = 31
+    U = gen.lap2d(N)
+    i = np.arange(1, N + 1)
+    x = np.outer(np.sin(p * np.pi * i / (N + 1)), np.sin(q * np.pi * i / (N + 1))).ravel()
+    lam = 4 - 2 * math.cos(p * math.pi / (N + 1)) - 2 * math.cos(q * math.pi / (N + 1))
+    Y = oracle.matrix_powers(U, x, 5)
+    for k in range(1, 6):
+        err = np.max(np.abs(Y[k - 1] - lam ** k * x))
+        assert err <= 32 * k * U_EPS * (8.0 + abs(lam)) ** k * np.max(np.abs(x)), (k, err)
+        # a dropped transposed term or a missing power leaves O(lambda^(k-1)) errors
+        assert err < 1e-3 * abs(lam) ** (k - 1) * np.max(np.abs(x))
+
+
+def test_matrix_powers_degenerate():
+    U = gen.lap2d(6)
+    x = np.random.default_rng(8).uniform(-1, 1, U.n)
+    assert oracle.matrix_powers(U, x, 0).shape == (0, U.n)
+    # diagonal-only matrix: A^k x = d^k x elementwise
+    D = gen.from_edges(5, [], [], [], diag=[2.0, -1.0, 0.5, 3.0, 1.0])
+    xd = np.array([1.0, 2.0, -1.0, 0.5, 4.0])
+    d = np.array([2.0, -1.0, 0.5, 3.0, 1.0])
+    Y = oracle.matrix_powers(D, xd, 3)
+    for k in range(1, 4):
+        assert np.array_equal(Y[k - 1], d ** k * xd)
