@@ -87,7 +87,9 @@ typedef struct {
   int32_t validate;         /* 1 = run the write-set stamping validator (always cheap)       */
   uint32_t flags;           /* bit 0: within-level order = original index (experimental);
                                bit 1: tile phases follow the stage-0 colours (red groups' tiles,
-                               then blue, greedy; default for scheme 0 is DSatur over all tiles) */
+                               then blue, greedy; default for scheme 0 is DSatur over all tiles);
+                               bit 2: keep the DSatur colour sizes (default: rebalanced towards
+                               equal phase sizes, a proper colouring still) */
   int32_t scheme;           /* 0 = RACE (levels, groups, tiles: the default);
                                3 = RACE with the recursive tree (§4.4.1-4.4.2):
                                    level groups with > 1 worker refined stage by stage on their

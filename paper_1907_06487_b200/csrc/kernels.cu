@@ -56,6 +56,10 @@ __device__ __forceinline__ void red_add_f64(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_add_u32(unsigned int* p, unsigned int v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int V>
 __device__ __forceinline__ double group_sum(double s) {
 #pragma unroll
@@ -465,7 +469,10 @@ __device__ __forceinline__ void group_sync(int g) {
 constexpr int kZeroThreads = kTiledThreads - 32;
 __device__ __forceinline__ void k4_zero_y(const K8Args* z, double* y, int G, int ztid,
                                           unsigned long long* s_target) {
-  const int64_t zb = z->zero_begin, zn = z->zero_end - zb;
+  // rounds mode (z->zround): the prologue zeroes rounds 0 .. kZeroLookahead only
+  const int nlead = z->zround != nullptr ? min(kZeroLookahead, z->nrounds - 1) : -1;
+  const int64_t zb = z->zround != nullptr ? z->zr[0] : z->zero_begin;
+  const int64_t zn = (z->zround != nullptr ? z->zr[nlead + 1] : z->zero_end) - zb;
   const int64_t per = ((zn + G - 1) / G + 1) & ~int64_t(1);
   int64_t a = zb + (int64_t)blockIdx.x * per;
   const int64_t e = min(zb + zn, a + per);
@@ -481,9 +488,27 @@ __device__ __forceinline__ void k4_zero_y(const K8Args* z, double* y, int G, int
   if (ztid == 0) {
     __threadfence();
     *s_target = (z->zero_dbg & 2) ? 0ull : (atomicAdd(z->zero_ctr, 1ull) / (unsigned)G + 1) * (unsigned)G;
+    for (int i = 0; i <= nlead; ++i) atomicAdd(z->zround + i, 1ull);
   }
   asm volatile("bar.sync 1, %0;" ::"n"(kZeroThreads) : "memory");
 }
+// K4 zeroing in rounds (large y; capi.cpp build_round_zero): the CTA's 1/G
+// share of the rows of round i, stored by the threads of one consumer group
+template <int NT>
+__device__ __forceinline__ void k4_round_zero(const K8Args* z, double* y, int G, int i, int gt) {
+  const int64_t zb = z->zr[i], zn = z->zr[i + 1] - zb;
+  const int64_t per = ((zn + G - 1) / G + 1) & ~int64_t(1);
+  int64_t a = zb + (int64_t)blockIdx.x * per;
+  const int64_t e = min(zb + zn, a + per);
+  if (a >= e) return;
+  if (((uintptr_t)(y + a) & 15) && gt == 0) y[a] = 0.0;
+  a += ((uintptr_t)(y + a) & 15) ? 1 : 0;
+  const int64_t nb = (e - a) / 2;
+  double2* y2 = reinterpret_cast<double2*>(y + a);
+  for (int64_t q = gt; q < nb; q += NT) y2[q] = make_double2(0.0, 0.0);
+  if (gt == 0 && a + 2 * nb < e) y[e - 1] = 0.0;
+}
+
 // one poller per warp, once per launch
 __device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long t) {
   if ((threadIdx.x & 31) == 0)
@@ -524,33 +549,52 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   }
   __syncthreads();
   __shared__ unsigned long long zero_target;
-  const bool self_zero = ATOMIC && A.k8->zero_ctr != nullptr;
-  if (self_zero && wid != kGroups * kGroupWarps) {
+  // K4 y zeroing: prologue (small y) or in rounds just ahead of the tiles
+  // (large y, k4_round_zero)
+  const bool stream_zero = ATOMIC && A.k8->zround != nullptr;
+  const bool self_zero = ATOMIC && A.k8->zero_ctr != nullptr && !stream_zero;
+  if ((self_zero || stream_zero) && wid != kGroups * kGroupWarps) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel of the stream is done
     k4_zero_y(A.k8, y, G, wid < kGroups * kGroupWarps ? tid : tid - 32, &zero_target);
   }
   if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
-    // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
+    // lane 0 issues; (offset, bytes) of the next 4 tiles of this CTA live in a
     // register ring (loop unrolled by 4) so each issue finds its operands ready.
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
-      int T0 = 0, T1 = 0, T2 = 0, T3 = 0;
-      auto ld = [&](int kk, int4& d, int& T) {
-        const int tt = blockIdx.x + kk * G;
-        if (tt < A.ntiles) {
-          const TileDesc& D = A.tiles[ORDERED ? __ldg(A.k8->order + tt) : tt];
-          const int64_t o = D.block_off;
-          d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
-          T = D.nrows;
+    // K4 rounds mode: before the first tile of round j >= 1 the whole warp
+    // zeroes this CTA's share of round j + L and counts it (the loader has no
+    // REDs in flight, so its fence is short; it runs NS tiles ahead of the
+    // consumers and mostly waits for free stages anyway).
+    const uint64_t pol = policy_evict_first();
+    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
+    int T0 = 0, T1 = 0, T2 = 0, T3 = 0;
+    bool waited = false;  // griddepcontrol.wait done (before the first y store)
+    auto ld = [&](int kk, int4& d, int& T) {
+      const int tt = blockIdx.x + kk * G;
+      if (lane == 0 && tt < A.ntiles) {
+        const TileDesc& D = A.tiles[ORDERED ? __ldg(A.k8->order + tt) : tt];
+        const int64_t o = D.block_off;
+        d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
+        T = D.nrows;
+      }
+    };
+    auto issue = [&](int k, int4 d, int T) {
+      if (stream_zero && k > 0 && k % A.k8->round_tiles == 0) {
+        const int i = k / A.k8->round_tiles + kZeroLookahead;
+        if (i < A.k8->nrounds) {
+          if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+          }
+          k4_round_zero<32>(A.k8, y, G, i, lane);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) atomicAdd(A.k8->zround + i, 1ull);
         }
-      };
-      auto issue = [&](int k, int4 d, int T) {
+      }
+      if (lane == 0) {
         const int s = k % NS, use = k / NS;
         const int64_t off = (int64_t)(uint32_t)d.x | ((int64_t)d.y << 32);
-        const int row0 = d.w;
-        (void)row0;
         (void)T;
         TRACE(k, 6);
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
@@ -562,24 +606,39 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z);
         bulk_g2s_stream(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s], pol);
         TRACE(k, 0);
-      };
-      ld(0, d0, T0);
-      ld(1, d1, T1);
-      ld(2, d2, T2);
-      ld(3, d3, T3);
-      const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
-      for (int kb = 0; kb < nk; kb += 4) {
-        issue(kb, d0, T0);
-        ld(kb + 4, d0, T0);
-        if (kb + 1 >= nk) break;
-        issue(kb + 1, d1, T1);
-        ld(kb + 5, d1, T1);
-        if (kb + 2 >= nk) break;
-        issue(kb + 2, d2, T2);
-        ld(kb + 6, d2, T2);
-        if (kb + 3 >= nk) break;
-        issue(kb + 3, d3, T3);
-        ld(kb + 7, d3, T3);
+      }
+      __syncwarp();
+    };
+    ld(0, d0, T0);
+    ld(1, d1, T1);
+    ld(2, d2, T2);
+    ld(3, d3, T3);
+    const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
+    for (int kb = 0; kb < nk; kb += 4) {
+      issue(kb, d0, T0);
+      ld(kb + 4, d0, T0);
+      if (kb + 1 >= nk) break;
+      issue(kb + 1, d1, T1);
+      ld(kb + 5, d1, T1);
+      if (kb + 2 >= nk) break;
+      issue(kb + 2, d2, T2);
+      ld(kb + 6, d2, T2);
+      if (kb + 3 >= nk) break;
+      issue(kb + 3, d3, T3);
+      ld(kb + 7, d3, T3);
+    }
+    // rounds whose first tile this CTA never reaches: zero its share anyway
+    if (stream_zero) {
+      const int j0 = (nk + A.k8->round_tiles - 1) / A.k8->round_tiles;  // first round without a tile here
+      for (int i = max(j0, 1) + kZeroLookahead; i < A.k8->nrounds; ++i) {
+        if (!waited) {
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          waited = true;
+        }
+        k4_round_zero<32>(A.k8, y, G, i, lane);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) atomicAdd(A.k8->zround + i, 1ull);
       }
     }
     return;
@@ -601,6 +660,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
       const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
       const int gruns = __ldg(&Dg->gather_runs) && !(K4_DBG & 8);
+
       // the first batch of run records (8 per lane) is loaded before the stage
       // wait, so its latency overlaps it
       int4 R[8];
@@ -694,6 +754,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // K4: zero this CTA's slice of y while the loader fills the ring; the first
   // flush of every warp waits until all CTAs have zeroed theirs (zero_ctr)
   bool zero_pending = self_zero;
+  int zr_ready = -1;             // K4 rounds: the last round this warp has seen zeroed
+  unsigned long long zpre = 0;   // ... and zround[zr_ready + 1], loaded ahead (lane 0)
+  int k8_prev = -1;  // K8: the tile this warp flushed last, signalled after the next tile's sums
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
@@ -726,19 +789,35 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // stored, spill contributions staged
     const int tile_id = ORDERED ? __ldg(A.k8->order + t) : t;
     if constexpr (ORDERED) {
-      // K8: the slot sums of this thread first (registers, at most kK8Slots:
-      // the plan checks window_cap), then the wait for the tile's DAG
-      // predecessors, then the flush.  The sums of tile k overlap the flushes
-      // of its predecessors: only the flush is on the DAG's critical path.
+      // K8, software-pipelined so that no L2 round trip sits between two
+      // tiles of a group:
+      //   1. acquire loads of this tile's DAG predecessors' flush counters
+      //      (issued now, inspected after the sums);
+      //   2. the slot sums in registers (at most kK8Slots per thread: the plan
+      //      checks window_cap), flush targets and first-writer flags;
+      //   3. the stage is released (nothing below reads it);
+      //   4. the PREVIOUS tile of this warp is signalled (its flush was issued
+      //      one tile ago, so the release fence finds it acknowledged);
+      //   5. wait until every predecessor has flushed (normally already true);
+      //   6. flush: the first writer of a target (lowest phase) stores, later
+      //      writers add with RED in DAG (= phase) order -- one writer at a time
+      //      per target, so the sum order is fixed and the result bitwise
+      //      reproducible; no old-value loads, nothing to wait for.
+      const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
+      unsigned pv = (unsigned)kGroupWarps;
+      if (pb + lane < pe && !(K4_DBG & 16)) pv = ld_acquire_u32(A.k8->done + __ldg(A.k8->dag_pred + pb + lane));
       double acc8[kK8Slots];
-      int l8[kK8Slots];
+      int gr8[kK8Slots];
+      bool st8[kK8Slots];
 #pragma unroll
       for (int u = 0; u < kK8Slots; ++u) {
         const int i = gt + u * kGroupThreads;
         acc8[u] = 0.0;
-        l8[u] = -1;
+        gr8[u] = -1;
+        st8[u] = false;
         if (i < W) {
           double acc = 0.0;
+          int l;
           if (!D.sorted) {
             if (i < T) {
               const uint32_t sg = rseg[i];
@@ -752,7 +831,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
               const uint32_t q = tcsc[j];
               acc += val[q & 0xffffu] * xs[q >> 16];
             }
-            l8[u] = i;
+            l = i;
           } else {
             const uint32_t* pseg = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
             const uint32_t* rec = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
@@ -763,48 +842,49 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
               const uint32_t q = rec[jb + v];
               acc += val[q & 0xffffu] * xs[q >> 16];
             }
-            l8[u] = sid[i];
+            l = sid[i];
           }
           acc8[u] = acc;
-        }
-      }
-      if (!(K4_DBG & 16)) {  // (bit 4: diagnostics, no DAG wait)
-        const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
-        for (int q = pb + lane; q < pe; q += 32) {
-          const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
-          while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(32);
-        }
-        __syncwarp();
-        __threadfence();
-      }
-      // flush: the first writer of a target (lowest phase) stores, later ones
-      // add in phase order (the DAG); the old values of all of this thread's
-      // targets are loaded before the first store
-      int gr8[kK8Slots];
-      double old8[kK8Slots];
-#pragma unroll
-      for (int u = 0; u < kK8Slots; ++u) {
-        const int l = l8[u];
-        gr8[u] = -1;
-        old8[u] = 0.0;
-        if (l >= 0) {
-          bool first;
           if (l < T) {
             gr8[u] = row0 + l;
-            first = __ldg(A.k8->own_first + row0 + l) != 0;
+            st8[u] = __ldg(A.k8->own_first + row0 + l) != 0;
           } else {
             gr8[u] = tgt[l - T];
-            first = gr8[u] >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
+            st8[u] = gr8[u] >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
           }
-          if (gr8[u] >= 0 && !first && !(K4_DBG & 32)) old8[u] = __ldcg(y + gr8[u]);  // (bit 5: no RMW)
-          else if (gr8[u] >= 0) l8[u] = -2;  // store
         }
       }
-      if (!(K4_DBG & 4)) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_relaxed(&empty[s]);  // 3. the stage is free
+      if (k8_prev >= 0) {                              // 4. signal the previous tile
+        if (!(K4_DBG & 64)) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // (bit 6: diagnostics, no fence)
+        __syncwarp();
+        if (lane == 0) red_add_u32(A.k8->done + k8_prev, 1u);
+      }
+      if (!(K4_DBG & 16)) {  // 5. (bit 4: diagnostics, no DAG wait)
+        if (!__all_sync(0xffffffffu, pv >= (unsigned)kGroupWarps)) {
+          for (int q = pb + lane; q < pe; q += 32) {
+            const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
+            while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(32);
+          }
+          __syncwarp();
+        } else {
+          for (int q = pb + 32 + lane; q < pe; q += 32) {  // (tiles with > 32 predecessors)
+            const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
+            while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(32);
+          }
+          __syncwarp();
+        }
+      }
+      if (!(K4_DBG & 4)) {  // 6.
 #pragma unroll
         for (int u = 0; u < kK8Slots; ++u)
-          if (gr8[u] >= 0) __stcg(y + gr8[u], l8[u] == -2 ? acc8[u] : old8[u] + acc8[u]);
+          if (gr8[u] >= 0) {
+            if (st8[u] || (K4_DBG & 32)) __stcg(y + gr8[u], acc8[u]);
+            else red_add_f64(y + gr8[u], acc8[u]);
+          }
       }
+      k8_prev = tile_id;
     } else {
     auto flush = [&](int l, int sl, double acc) {
       if (K4_DBG & 4) {
@@ -828,6 +908,26 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     if (zero_pending) {  // first tile of this warp: every CTA has zeroed its slice of y
       k4_zero_wait(A.k8, zero_target);
       zero_pending = false;
+    }
+    if (stream_zero) {
+      // a tile of round j flushes once every CTA has zeroed its share of
+      // round j (prologue: rounds 0 .. L; the loader warps: later rounds)
+      const int j = k / A.k8->round_tiles;
+      const unsigned long long tgt_cnt = zero_target;
+      if (zr_ready < j) {
+        // zpre: zround[j] as loaded (acquire) one round ago -- normally
+        // complete already, so no L2 round trip sits in front of the tile
+        if (lane == 0) {
+          if (zr_ready != j - 1) zpre = 0;
+          while (zpre < tgt_cnt) {
+            zpre = ld_acquire_u64(A.k8->zround + j);
+            if (zpre < tgt_cnt) __nanosleep(64);
+          }
+          zpre = j + 1 < A.k8->nrounds ? ld_acquire_u64(A.k8->zround + j + 1) : 0ull;
+        }
+        __syncwarp();
+        zr_ready = j;
+      }
     }
     if (!D.sorted) {
       // slot order: a warp walks the row parts of 32 consecutive slots in
@@ -872,15 +972,18 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     }
     }  // !ORDERED
     if (gt == 0) TRACE(k, 4);
-    if (ORDERED) {  // this warp's stores of the tile are visible: count it
-      __threadfence();
+    if (!ORDERED) {
+      // release stage s: each warp arrives once its reads of the stage are done
+      // (K8 released it before its flush)
       __syncwarp();
-      if (lane == 0) atomicAdd(A.k8->done + tile_id, 1u);
+      if (lane == 0) mbar_arrive_relaxed(&empty[s]);
     }
-    // release stage s: each warp arrives once its reads of the stage are done
-    __syncwarp();
-    if (lane == 0) mbar_arrive_relaxed(&empty[s]);
     if (gt == 0) TRACE(k, 5);
+  }
+  if (ORDERED && k8_prev >= 0) {  // signal this warp's last tile
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) red_add_u32(A.k8->done + k8_prev, 1u);
   }
 }
 

@@ -1088,6 +1088,41 @@ int build_schedule(const symm_csr_upper* U, const race_config* cfgp, Schedule* S
     }
     { std::vector<std::vector<uint64_t>>().swap(sat); }
     ncol[0] = nc;
+    // Equitable rebalancing (flags bit 2 turns it off).  DSatur fills the
+    // first colours greedily, so the last ones are small (st27_128: 2281 ...
+    // 39, 1 tiles).  K8 runs the phases in order with every tile waiting for
+    // its conflicting tiles of earlier phases: small phases at the end form a
+    // chain with less than one wave of tiles per link, and a tile at the start
+    // of a phase finds its predecessors less than one wave back.  A tile moves
+    // from a colour above the mean size to the smallest colour that none of its
+    // conflicting tiles has, if that colour is smaller by two or more; sweeps
+    // in id order until nothing moves.  The colouring stays proper.
+    if (!(cfg.flags & 4u) && nc > 1) {
+      std::vector<int64_t> size((size_t)nc, 0);
+      for (int32_t t = 0; t < ntiles; ++t) size[(size_t)tcol[(size_t)t]]++;
+      const int64_t target = (ntiles + nc - 1) / nc;
+      std::vector<int32_t> seen((size_t)nc, -1);
+      for (int sweep = 0; sweep < 16; ++sweep) {
+        int64_t moved = 0;
+        for (int32_t t = 0; t < ntiles; ++t) {
+          const int32_t c = tcol[(size_t)t];
+          if (size[(size_t)c] <= target) continue;
+          for (int32_t u : conf[(size_t)t]) seen[(size_t)tcol[(size_t)u]] = t;
+          int32_t best = -1;
+          for (int32_t d = 0; d < nc; ++d)
+            if (seen[(size_t)d] != t && d != c && size[(size_t)d] + 2 <= size[(size_t)c] &&
+                (best < 0 || size[(size_t)d] < size[(size_t)best]))
+              best = d;
+          if (best >= 0) {
+            tcol[(size_t)t] = best;
+            size[(size_t)c]--;
+            size[(size_t)best]++;
+            ++moved;
+          }
+        }
+        if (moved == 0) break;
+      }
+    }
   }
   for (int32_t t = 0; t < ntiles && !dsatur; ++t) {
     int32_t s0 = S->tile_group[(size_t)t] % 2;
