@@ -72,7 +72,6 @@ struct symmspmv_plan {
   // K8 tiled_colored
   bool has_tiled_colored = false;
   bool k4_self_zero = true;         // k_tiled<1> zeroes y itself (no k_zero launch)
-  bool k4_stream_zero = false;      // ... chunk by chunk just ahead of its writers (large y)
   unsigned int* k8_done = nullptr;  // host copy of the counters' address (memset per run)
   // K7 recursive tree
   bool has_tree = false;
@@ -744,50 +743,6 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
   return SYMM_OK;
 }
 
-// K4 zeroing of a large y in rounds (single-rank plans whose y exceeds half
-// the L2).  A k_zero launch writes 8n bytes of zeros to DRAM that the REDs then
-// read back (the zeros do not fit in the L2): y costs 24n bytes of DRAM
-// traffic.  Here the CTAs zero y in rounds just ahead of the tiles that write
-// it, so the zeros are still in L2 when the REDs arrive and y costs one DRAM
-// write (8n).  Tiles are processed in id order per CTA (tile k of CTA c is
-// c + k G); round j holds the tiles with k in [16 j, 16 (j+1)) (16 = kZeroRoundTiles), and its zero
-// range [zr[j], zr[j+1]) ends at the last row any tile of rounds <= j writes
-// (own rows or spill targets), so a tile of round j writes only rows of
-// rounds <= j.  A CTA zeroes its 1/G share of round j + 2 when it starts
-// round j (rounds 0..2 when it starts) and then adds 1 to zround[j + 2]; a
-// tile of round j flushes after zround[j] has reached (launch + 1) G.  Every
-// CTA zeroes its shares in round order before it waits in that round, so the
-// waits cannot deadlock (all CTAs are resident: grid <= SMs, 1 CTA per SM).
-int build_round_zero(symmspmv_plan_t* P, const Schedule& S, const TiledHost& H, int grid, K8Args& k8h) {
-  const int32_t ntl = (int32_t)H.desc.size();
-  int32_t rt = kZeroRoundTiles;
-  if (const char* e = std::getenv("SYMM_ZERO_ROUND")) rt = std::max(8, std::atoi(e));  // > ring depth (<= 8)
-  const int64_t per = (int64_t)rt * grid;
-  const int32_t nr = (int32_t)((ntl + per - 1) / per);
-  std::vector<int64_t> zr((size_t)nr + 1, P->row_begin);
-  int64_t m = P->row_begin;
-  for (int32_t i = 0; i < ntl; ++i) {
-    const TileDesc& D = H.desc[(size_t)i];
-    int64_t hi = (int64_t)D.row0 + D.nrows;
-    const int64_t a = S.spill_ptr[(size_t)i], b = S.spill_ptr[(size_t)i + 1];
-    for (int64_t q = a; q < b; ++q) hi = std::max<int64_t>(hi, (int64_t)((uint32_t)S.spill[(size_t)q] & kIdxMask) + 1);
-    m = std::max(m, hi);
-    zr[(size_t)(i / per) + 1] = m;
-  }
-  if (zr[(size_t)nr] != P->local_end) return set_error(SYMM_ERR_SCHEDULE, "round zero: rows [%lld, %d) have no writer", (long long)zr[(size_t)nr], P->local_end);
-  int64_t* d_zr;
-  unsigned long long* d_zc;
-  int rc;
-  if ((rc = upload(P, &d_zr, zr.data(), zr.size())) || (rc = dev_alloc(P, &d_zc, (size_t)nr))) return rc;
-  if (cudaError_t e = cudaMemset(d_zc, 0, sizeof(unsigned long long) * (size_t)nr)) return cuda_fail(e, "zero round counters");
-  k8h.zr = d_zr;
-  k8h.zround = d_zc;
-  k8h.nrounds = nr;
-  k8h.round_tiles = rt;
-  P->k4_stream_zero = true;
-  return SYMM_OK;
-}
-
 int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t t_end) {
   TiledHost H;
   if (int rc = build_tiled_host(S, t_begin, t_end, H)) return rc;
@@ -871,15 +826,10 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, P->device);
     const int64_t ybytes = 8 * ((int64_t)P->local_end - P->row_begin);
-    // mode 1: prologue zeroing (y <= L2/2); 2: zeroing in rounds (single-rank
-    // plans with a large y); 0: a k_zero launch before the kernel
-    // (mode 2 measured slower than mode 0 on lap3d_512 so far: opt-in, SYMM_K4_ZERO=2)
-    int zmode = ybytes <= (int64_t)l2 / 2 ? 1 : 0;
-    if (const char* e = std::getenv("SYMM_K4_ZERO")) zmode = std::atoi(e);
-    if (zmode == 2 && !(P->nranks == 1 && ntl > 0)) zmode = 0;
-    k8h.zero_ctr = zmode != 0 ? d_zc : nullptr;
-    P->k4_self_zero = zmode != 0;
-    if (zmode == 2 && (rc = build_round_zero(P, S, H, std::max(1, std::min(P->sms, ntl)), k8h))) return rc;
+    bool self_zero = ybytes <= (int64_t)l2 / 2;
+    if (const char* e = std::getenv("SYMM_K4_ZERO")) self_zero = std::atoi(e) != 0;
+    k8h.zero_ctr = self_zero ? d_zc : nullptr;
+    P->k4_self_zero = self_zero;
   }
   k8h.zero_begin = P->row_begin;
   k8h.zero_end = P->local_end;

@@ -149,20 +149,7 @@ struct K8Args {                   // (K3 / K8 tables, device memory)
   unsigned long long* zero_ctr;   // nullptr: y is zeroed by k_zero before the launch
   int64_t zero_begin, zero_end;   // global row ids of the local y range
   int32_t zero_dbg;               // diagnostics (env SYMM_ZERO_DBG): bit0 no stores, bit1 no wait
-  // K4 zeroing of a large y in rounds (capi.cpp build_round_zero; zround ==
-  // nullptr: off).  Round j = the tiles with CTA-local index k in
-  // [j round_tiles, (j+1) round_tiles); its rows to zero are
-  // [zr[j], zr[j+1]); every CTA zeroes its share of round j + kZeroLookahead
-  // when it starts round j (rounds 0 .. kZeroLookahead at its start) and
-  // counts it in zround; a tile of round j flushes once zround[j] shows every
-  // CTA of this launch.
-  const int64_t* zr;              // [nrounds+1] row boundaries (global row ids)
-  unsigned long long* zround;     // [nrounds] +gridDim.x per launch, never reset
-  int32_t nrounds;
-  int32_t round_tiles;            // tiles per CTA per round (default kZeroRoundTiles, > ring depth)
 };
-constexpr int kZeroRoundTiles = 16;  // tiles per CTA per zeroing round (env SYMM_ZERO_ROUND, >= 8)
-constexpr int kZeroLookahead = 2;    // rounds zeroed ahead of their tiles
 
 
 struct TiledArgs {

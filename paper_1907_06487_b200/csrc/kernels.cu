@@ -469,10 +469,7 @@ __device__ __forceinline__ void group_sync(int g) {
 constexpr int kZeroThreads = kTiledThreads - 32;
 __device__ __forceinline__ void k4_zero_y(const K8Args* z, double* y, int G, int ztid,
                                           unsigned long long* s_target) {
-  // rounds mode (z->zround): the prologue zeroes rounds 0 .. kZeroLookahead only
-  const int nlead = z->zround != nullptr ? min(kZeroLookahead, z->nrounds - 1) : -1;
-  const int64_t zb = z->zround != nullptr ? z->zr[0] : z->zero_begin;
-  const int64_t zn = (z->zround != nullptr ? z->zr[nlead + 1] : z->zero_end) - zb;
+  const int64_t zb = z->zero_begin, zn = z->zero_end - zb;
   const int64_t per = ((zn + G - 1) / G + 1) & ~int64_t(1);
   int64_t a = zb + (int64_t)blockIdx.x * per;
   const int64_t e = min(zb + zn, a + per);
@@ -488,27 +485,9 @@ __device__ __forceinline__ void k4_zero_y(const K8Args* z, double* y, int G, int
   if (ztid == 0) {
     __threadfence();
     *s_target = (z->zero_dbg & 2) ? 0ull : (atomicAdd(z->zero_ctr, 1ull) / (unsigned)G + 1) * (unsigned)G;
-    for (int i = 0; i <= nlead; ++i) atomicAdd(z->zround + i, 1ull);
   }
   asm volatile("bar.sync 1, %0;" ::"n"(kZeroThreads) : "memory");
 }
-// K4 zeroing in rounds (large y; capi.cpp build_round_zero): the CTA's 1/G
-// share of the rows of round i, stored by the threads of one consumer group
-template <int NT>
-__device__ __forceinline__ void k4_round_zero(const K8Args* z, double* y, int G, int i, int gt) {
-  const int64_t zb = z->zr[i], zn = z->zr[i + 1] - zb;
-  const int64_t per = ((zn + G - 1) / G + 1) & ~int64_t(1);
-  int64_t a = zb + (int64_t)blockIdx.x * per;
-  const int64_t e = min(zb + zn, a + per);
-  if (a >= e) return;
-  if (((uintptr_t)(y + a) & 15) && gt == 0) y[a] = 0.0;
-  a += ((uintptr_t)(y + a) & 15) ? 1 : 0;
-  const int64_t nb = (e - a) / 2;
-  double2* y2 = reinterpret_cast<double2*>(y + a);
-  for (int64_t q = gt; q < nb; q += NT) y2[q] = make_double2(0.0, 0.0);
-  if (gt == 0 && a + 2 * nb < e) y[e - 1] = 0.0;
-}
-
 // one poller per warp, once per launch
 __device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long t) {
   if ((threadIdx.x & 31) == 0)
@@ -535,6 +514,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t blk_full[NS], x_full[NS], empty[NS];
   __shared__ int loader_k;  // tiles the loader has taken a free stage for (gather warps follow it)
+  // K8: warps of a group done flushing a tile (mod 7), by group tile index mod
+  // 4 (the warps of a group are at most two group tiles apart: the stage ring)
+  __shared__ unsigned k8_arrive[kGroups][4];
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
@@ -546,55 +528,37 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     loader_k = 0;
+    for (int q = 0; q < kGroups * 4; ++q) k8_arrive[q / 4][q % 4] = 0;
   }
   __syncthreads();
   __shared__ unsigned long long zero_target;
-  // K4 y zeroing: prologue (small y) or in rounds just ahead of the tiles
-  // (large y, k4_round_zero)
-  const bool stream_zero = ATOMIC && A.k8->zround != nullptr;
-  const bool self_zero = ATOMIC && A.k8->zero_ctr != nullptr && !stream_zero;
-  if ((self_zero || stream_zero) && wid != kGroups * kGroupWarps) {
+  const bool self_zero = ATOMIC && A.k8->zero_ctr != nullptr;
+  if (self_zero && wid != kGroups * kGroupWarps) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel of the stream is done
     k4_zero_y(A.k8, y, G, wid < kGroups * kGroupWarps ? tid : tid - 32, &zero_target);
   }
   if (wid == kGroups * kGroupWarps) {
     // ------------------------------------------------ loader warp (TMA bulk)
-    // lane 0 issues; (offset, bytes) of the next 4 tiles of this CTA live in a
+    // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
     // register ring (loop unrolled by 4) so each issue finds its operands ready.
-    // K4 rounds mode: before the first tile of round j >= 1 the whole warp
-    // zeroes this CTA's share of round j + L and counts it (the loader has no
-    // REDs in flight, so its fence is short; it runs NS tiles ahead of the
-    // consumers and mostly waits for free stages anyway).
-    const uint64_t pol = policy_evict_first();
-    int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
-    int T0 = 0, T1 = 0, T2 = 0, T3 = 0;
-    bool waited = false;  // griddepcontrol.wait done (before the first y store)
-    auto ld = [&](int kk, int4& d, int& T) {
-      const int tt = blockIdx.x + kk * G;
-      if (lane == 0 && tt < A.ntiles) {
-        const TileDesc& D = A.tiles[ORDERED ? __ldg(A.k8->order + tt) : tt];
-        const int64_t o = D.block_off;
-        d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
-        T = D.nrows;
-      }
-    };
-    auto issue = [&](int k, int4 d, int T) {
-      if (stream_zero && k > 0 && k % A.k8->round_tiles == 0) {
-        const int i = k / A.k8->round_tiles + kZeroLookahead;
-        if (i < A.k8->nrounds) {
-          if (!waited) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            waited = true;
-          }
-          k4_round_zero<32>(A.k8, y, G, i, lane);
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) atomicAdd(A.k8->zround + i, 1ull);
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
+      int T0 = 0, T1 = 0, T2 = 0, T3 = 0;
+      auto ld = [&](int kk, int4& d, int& T) {
+        const int tt = blockIdx.x + kk * G;
+        if (tt < A.ntiles) {
+          const TileDesc& D = A.tiles[ORDERED ? __ldg(A.k8->order + tt) : tt];
+          const int64_t o = D.block_off;
+          d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
+          T = D.nrows;
         }
-      }
-      if (lane == 0) {
+      };
+      auto issue = [&](int k, int4 d, int T) {
         const int s = k % NS, use = k / NS;
         const int64_t off = (int64_t)(uint32_t)d.x | ((int64_t)d.y << 32);
+        const int row0 = d.w;
+        (void)row0;
         (void)T;
         TRACE(k, 6);
         if (use > 0) mbar_wait(&empty[s], (unsigned)((use - 1) & 1));
@@ -606,39 +570,24 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         mbar_arrive_expect_tx(&blk_full[s], (unsigned)d.z);
         bulk_g2s_stream(sm + s * slot_bytes, A.blocks + off, (unsigned)d.z, &blk_full[s], pol);
         TRACE(k, 0);
-      }
-      __syncwarp();
-    };
-    ld(0, d0, T0);
-    ld(1, d1, T1);
-    ld(2, d2, T2);
-    ld(3, d3, T3);
-    const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
-    for (int kb = 0; kb < nk; kb += 4) {
-      issue(kb, d0, T0);
-      ld(kb + 4, d0, T0);
-      if (kb + 1 >= nk) break;
-      issue(kb + 1, d1, T1);
-      ld(kb + 5, d1, T1);
-      if (kb + 2 >= nk) break;
-      issue(kb + 2, d2, T2);
-      ld(kb + 6, d2, T2);
-      if (kb + 3 >= nk) break;
-      issue(kb + 3, d3, T3);
-      ld(kb + 7, d3, T3);
-    }
-    // rounds whose first tile this CTA never reaches: zero its share anyway
-    if (stream_zero) {
-      const int j0 = (nk + A.k8->round_tiles - 1) / A.k8->round_tiles;  // first round without a tile here
-      for (int i = max(j0, 1) + kZeroLookahead; i < A.k8->nrounds; ++i) {
-        if (!waited) {
-          asm volatile("griddepcontrol.wait;" ::: "memory");
-          waited = true;
-        }
-        k4_round_zero<32>(A.k8, y, G, i, lane);
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) atomicAdd(A.k8->zround + i, 1ull);
+      };
+      ld(0, d0, T0);
+      ld(1, d1, T1);
+      ld(2, d2, T2);
+      ld(3, d3, T3);
+      const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
+      for (int kb = 0; kb < nk; kb += 4) {
+        issue(kb, d0, T0);
+        ld(kb + 4, d0, T0);
+        if (kb + 1 >= nk) break;
+        issue(kb + 1, d1, T1);
+        ld(kb + 5, d1, T1);
+        if (kb + 2 >= nk) break;
+        issue(kb + 2, d2, T2);
+        ld(kb + 6, d2, T2);
+        if (kb + 3 >= nk) break;
+        issue(kb + 3, d3, T3);
+        ld(kb + 7, d3, T3);
       }
     }
     return;
@@ -669,13 +618,22 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
         const int r = u * 32 + lane;
         R[u] = (gruns && r < nr) ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
       }
-      // stage free: the loader (which waits for the stages in order, so its
-      // parity waits cannot alias) has passed tile k
-      while (true) {
-        int lk;
-        asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(lk) : "r"(smem_u32(&loader_k)) : "memory");
-        if (lk > k) break;
-        __nanosleep(32);
+      // stage free: tile k - NS has been consumed.  With NS % kGatherWarps ==
+      // 0 an mbarrier wait (hardware suspend) replaces the poll of loader_k,
+      // which cost 9% of the kernel's shared-memory wavefronts on fem_knn_4M
+      // (ncu source page).  No parity alias: tile k - NS is this warp's own,
+      // and waiting for its stage it saw tile k - 2 NS consumed; tile k itself
+      // cannot be consumed yet.  Other ring depths poll loader_k (the loader
+      // waits for the stages in order, so its parity waits cannot alias).
+      if constexpr (NS % kGatherWarps == 0) {
+        if (k >= NS) mbar_wait(&empty[s], (unsigned)(((k / NS) - 1) & 1));
+      } else {
+        while (true) {
+          int lk;
+          asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(lk) : "r"(smem_u32(&loader_k)) : "memory");
+          if (lk > k) break;
+          __nanosleep(64);
+        }
       }
       if (lane == 0) TRACE(k, 1);
       const int p = (int)(((uintptr_t)(x + row0) >> 3) & 1);
@@ -754,21 +712,26 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // K4: zero this CTA's slice of y while the loader fills the ring; the first
   // flush of every warp waits until all CTAs have zeroed theirs (zero_ctr)
   bool zero_pending = self_zero;
-  int zr_ready = -1;             // K4 rounds: the last round this warp has seen zeroed
-  unsigned long long zpre = 0;   // ... and zround[zr_ready + 1], loaded ahead (lane 0)
-  int k8_prev = -1;  // K8: the tile this warp flushed last, signalled after the next tile's sums
   int k = g;
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
-    // The loader takes stages in order; only once it has taken the stage for
-    // tile k are the previous uses of blk_full[s] / x_full[s] complete, so a
-    // parity wait cannot alias a phase two uses back (a group may finish its
-    // previous tile before an older tile's block has landed).
-    while (true) {
-      int lk;
-      asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(lk) : "r"(smem_u32(&loader_k)) : "memory");
-      if (lk > k) break;
-      __nanosleep(32);
+    // The parity waits below are safe only once the previous use of stage s
+    // (tile k - NS) is complete: a group may finish its previous tile before
+    // an older tile's block has landed.  So wait first until tile k - NS has
+    // been consumed (empty[s], an mbarrier wait instead of a poll of
+    // loader_k).  No alias there either when NS >= kGroups: tile k - 2 NS is
+    // consumed (the loader issued this group's previous tile k - kGroups only
+    // after every tile <= k - kGroups - NS was consumed), and tile k cannot be
+    // yet.  Shallower rings poll loader_k.
+    if constexpr (NS >= kGroups) {
+      if (k >= NS) mbar_wait(&empty[s], (unsigned)(((k / NS) - 1) & 1));
+    } else {
+      while (true) {
+        int lk;
+        asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(lk) : "r"(smem_u32(&loader_k)) : "memory");
+        if (lk > k) break;
+        __nanosleep(32);
+      }
     }
     mbar_wait(&blk_full[s], (unsigned)((k / NS) & 1));  // TMA data visible to this thread
     mbar_wait(&x_full[s], (unsigned)((k / NS) & 1));
@@ -796,13 +759,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       //   2. the slot sums in registers (at most kK8Slots per thread: the plan
       //      checks window_cap), flush targets and first-writer flags;
       //   3. the stage is released (nothing below reads it);
-      //   4. the PREVIOUS tile of this warp is signalled (its flush was issued
-      //      one tile ago, so the release fence finds it acknowledged);
       //   5. wait until every predecessor has flushed (normally already true);
       //   6. flush: the first writer of a target (lowest phase) stores, later
       //      writers add with RED in DAG (= phase) order -- one writer at a time
       //      per target, so the sum order is fixed and the result bitwise
-      //      reproducible; no old-value loads, nothing to wait for.
+      //      reproducible; no old-value loads, nothing to wait for;
+      //   7. signal the tile (last arriving warp of the group).
       const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
       unsigned pv = (unsigned)kGroupWarps;
       if (pb + lane < pe && !(K4_DBG & 16)) pv = ld_acquire_u32(A.k8->done + __ldg(A.k8->dag_pred + pb + lane));
@@ -856,11 +818,6 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_relaxed(&empty[s]);  // 3. the stage is free
-      if (k8_prev >= 0) {                              // 4. signal the previous tile
-        if (!(K4_DBG & 64)) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // (bit 6: diagnostics, no fence)
-        __syncwarp();
-        if (lane == 0) red_add_u32(A.k8->done + k8_prev, 1u);
-      }
       if (!(K4_DBG & 16)) {  // 5. (bit 4: diagnostics, no DAG wait)
         if (!__all_sync(0xffffffffu, pv >= (unsigned)kGroupWarps)) {
           for (int q = pb + lane; q < pe; q += 32) {
@@ -884,7 +841,20 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
             else red_add_f64(y + gr8[u], acc8[u]);
           }
       }
-      k8_prev = tile_id;
+      // 7. signal: each warp arrives (release, CTA scope) on its group's
+      // counter for the tile; the last of the 7 makes the group's flush
+      // visible GPU-wide (one fence per tile instead of one per warp: the
+      // fence waits for the REDs in flight) and signals for all 7
+      __syncwarp();
+      if (lane == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old) : "r"(smem_u32(&k8_arrive[g][(k / kGroups) & 3])) : "memory");
+        if ((old + 1) % (unsigned)kGroupWarps == 0) {
+          if (!(K4_DBG & 64)) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // (bit 6: diagnostics, no fence)
+          red_add_u32(A.k8->done + tile_id, (unsigned)kGroupWarps);
+        }
+      }
     } else {
     auto flush = [&](int l, int sl, double acc) {
       if (K4_DBG & 4) {
@@ -908,26 +878,6 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     if (zero_pending) {  // first tile of this warp: every CTA has zeroed its slice of y
       k4_zero_wait(A.k8, zero_target);
       zero_pending = false;
-    }
-    if (stream_zero) {
-      // a tile of round j flushes once every CTA has zeroed its share of
-      // round j (prologue: rounds 0 .. L; the loader warps: later rounds)
-      const int j = k / A.k8->round_tiles;
-      const unsigned long long tgt_cnt = zero_target;
-      if (zr_ready < j) {
-        // zpre: zround[j] as loaded (acquire) one round ago -- normally
-        // complete already, so no L2 round trip sits in front of the tile
-        if (lane == 0) {
-          if (zr_ready != j - 1) zpre = 0;
-          while (zpre < tgt_cnt) {
-            zpre = ld_acquire_u64(A.k8->zround + j);
-            if (zpre < tgt_cnt) __nanosleep(64);
-          }
-          zpre = j + 1 < A.k8->nrounds ? ld_acquire_u64(A.k8->zround + j + 1) : 0ull;
-        }
-        __syncwarp();
-        zr_ready = j;
-      }
     }
     if (!D.sorted) {
       // slot order: a warp walks the row parts of 32 consecutive slots in
@@ -980,11 +930,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     }
     if (gt == 0) TRACE(k, 5);
   }
-  if (ORDERED && k8_prev >= 0) {  // signal this warp's last tile
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) red_add_u32(A.k8->done + k8_prev, 1u);
-  }
+
 }
 
 // K3 second kernel: y[r] += staged contributions of row r in slot order.
