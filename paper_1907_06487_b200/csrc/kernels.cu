@@ -505,6 +505,11 @@ __device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long
 #else
 #define K4_DBG 0
 #endif
+// K8: a dedicated signaller warp (the last gather warp) fences and signals
+// the DAG counters; 0 = the last-arriving consumer warp of a group does it
+#ifndef K8_SIGNALLER
+#define K8_SIGNALLER 1
+#endif
 template <int MODE, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
                                                             double* __restrict__ y) {
@@ -517,6 +522,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // K8: warps of a group done flushing a tile (mod 7), by group tile index mod
   // 4 (the warps of a group are at most two group tiles apart: the stage ring)
   __shared__ unsigned k8_arrive[kGroups][4];
+  // K8 with a signaller warp: tiles flushed by each consumer warp (release,
+  // CTA scope); the signaller turns them into the GPU-wide done[] counters
+  __shared__ unsigned k8_prog[kGroups * kGroupWarps];
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     loader_k = 0;
     for (int q = 0; q < kGroups * 4; ++q) k8_arrive[q / 4][q % 4] = 0;
+    for (int q = 0; q < kGroups * kGroupWarps; ++q) k8_prog[q] = 0;
   }
   __syncthreads();
   __shared__ unsigned long long zero_target;
@@ -601,9 +610,49 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // bulk copy (TMA) plus at most two 8-B cp.async edge elements; the lane also
     // copies the unaligned own-x edge elements (the loader bulk-copies the rest).
     const int gw = wid - (kGroups * kGroupWarps + 1);
+    if constexpr (ORDERED) {
+      if (K8_SIGNALLER && gw == kGatherWarps - 1) {
+        // ---------------------------------------------- K8 signaller warp
+        // Lane q < kGroups follows consumer group q.  A group tile j is
+        // flushed once all 7 warps of the group have published progress > j
+        // (st.release.cta after their REDs / stores).  Whenever tiles became
+        // complete, ONE fence.acq_rel.gpu (cumulative: it orders the REDs the
+        // acquire loads observed) precedes their done[] signals.  The consumer
+        // warps never wait for their REDs to reach L2 (that wait, one fence
+        // per tile on the consumers' path, was 26% of K8's time on st27).
+        const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
+        const int nq = (lane < kGroups && nk > lane) ? (nk - lane + kGroups - 1) / kGroups : 0;
+        int sig = 0;  // group tiles of lane q's group already signalled
+        while (__any_sync(0xffffffffu, sig < nq)) {
+          int m = nq;
+          if (sig < nq) {
+#pragma unroll
+            for (int w = 0; w < kGroupWarps; ++w) {
+              unsigned v;
+              asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+                           : "=r"(v) : "r"(smem_u32(&k8_prog[lane * kGroupWarps + w])) : "memory");
+              m = min(m, (int)v);
+            }
+          }
+          const bool any = __any_sync(0xffffffffu, m > sig);
+          if (!any) {
+            __nanosleep(64);
+            continue;
+          }
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          for (int j = sig; j < m; ++j) {
+            const int t = blockIdx.x + (lane + j * kGroups) * G;
+            red_add_u32(A.k8->done + __ldg(A.k8->order + t), (unsigned)kGroupWarps);
+          }
+          sig = max(sig, m);
+        }
+        return;
+      }
+    }
+    constexpr int NGW = (ORDERED && K8_SIGNALLER) ? kGatherWarps - 1 : kGatherWarps;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // x is ready (PDL prerequisite done)
     int k = gw;
-    for (int t = blockIdx.x + gw * G; t < A.ntiles; t += kGatherWarps * G, k += kGatherWarps) {
+    for (int t = blockIdx.x + gw * G; t < A.ntiles; t += NGW * G, k += NGW) {
       const int s = k % NS;
       const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(A.k8->order + t) : t);
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
@@ -625,7 +674,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       // and waiting for its stage it saw tile k - 2 NS consumed; tile k itself
       // cannot be consumed yet.  Other ring depths poll loader_k (the loader
       // waits for the stages in order, so its parity waits cannot alias).
-      if constexpr (NS % kGatherWarps == 0) {
+      if constexpr (NS % NGW == 0) {
         if (k >= NS) mbar_wait(&empty[s], (unsigned)(((k / NS) - 1) & 1));
       } else {
         while (true) {
@@ -846,7 +895,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       // visible GPU-wide (one fence per tile instead of one per warp: the
       // fence waits for the REDs in flight) and signals for all 7
       __syncwarp();
-      if (lane == 0) {
+      if (K8_SIGNALLER) {
+        // publish this warp's progress (group tiles flushed); the signaller
+        // warp fences and signals done[]
+        if (lane == 0)
+          asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&k8_prog[wid])), "r"(k / kGroups + 1)
+                       : "memory");
+      } else if (lane == 0) {
         unsigned old;
         asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(old) : "r"(smem_u32(&k8_arrive[g][(k / kGroups) & 3])) : "memory");
