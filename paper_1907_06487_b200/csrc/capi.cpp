@@ -793,17 +793,28 @@ int build_tiled(symmspmv_plan_t* P, const Schedule& S, int32_t t_begin, int32_t 
                      [&](int32_t a, int32_t b) { return S.tile_phase[(size_t)a] < S.tile_phase[(size_t)b]; });
     std::vector<int32_t> dq(S.dag_pred);
     if (dq.empty()) dq.push_back(0);
+    // per processing position: the tile and its predecessor range, one 16-B
+    // load (the consumers prefetch it a group tile ahead)
+    std::vector<int32_t> pm(4 * (size_t)ntl, 0);
+    for (int32_t q = 0; q < ntl; ++q) {
+      const int32_t id = order[(size_t)q];
+      pm[4 * (size_t)q] = id;
+      pm[4 * (size_t)q + 1] = S.dag_ptr[(size_t)id];
+      pm[4 * (size_t)q + 2] = S.dag_ptr[(size_t)id + 1];
+    }
+    int32_t* d_pm;
     int32_t *d_order, *d_dp, *d_dq;
     unsigned int* d_done;
     uint8_t *d_of, *d_sf;
     std::vector<uint8_t> of(S.own_first.begin(), S.own_first.end()), sf(H.slot_first.begin(), H.slot_first.end());
     if (sf.empty()) sf.push_back(0);
     if ((rc = upload(P, &d_of, of.data(), of.size())) || (rc = upload(P, &d_sf, sf.data(), sf.size())) ||
-        (rc = upload(P, &d_order, order.data(), order.size())) ||
+        (rc = upload(P, &d_order, order.data(), order.size())) || (rc = upload(P, &d_pm, pm.data(), pm.size())) ||
         (rc = upload(P, &d_dp, S.dag_ptr.data(), S.dag_ptr.size())) ||
         (rc = upload(P, &d_dq, dq.data(), dq.size())) || (rc = dev_alloc(P, &d_done, (size_t)std::max(ntl, 1))))
       return rc;
     k8h.order = d_order;
+    k8h.pos_meta = d_pm;
     k8h.dag_ptr = d_dp;
     k8h.dag_pred = d_dq;
     k8h.done = d_done;

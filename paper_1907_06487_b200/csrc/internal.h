@@ -141,6 +141,7 @@ struct K8Args {                   // (K3 / K8 tables, device memory)
   const int32_t* order;           // [ntiles] processing order -> tile id
   const int32_t* dag_ptr;         // [ntiles+1] predecessors of every tile id
   const int32_t* dag_pred;
+  const int32_t* pos_meta;        // [4 ntiles] by position: (tile id, dag_ptr[id], dag_ptr[id+1], 0), 16-B aligned
   unsigned int* done;             // [ntiles] warps of the owning group that flushed (zeroed per run)
   const uint8_t* own_first;       // [n] K8: the row's own tile writes it first (stores)
   const uint8_t* slot_first;      // [spill slots] K8: this spill slot's tile writes its target first

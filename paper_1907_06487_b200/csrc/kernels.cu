@@ -40,6 +40,11 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -507,6 +512,9 @@ __device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long
 #endif
 // K8: a dedicated signaller warp (the last gather warp) fences and signals
 // the DAG counters; 0 = the last-arriving consumer warp of a group does it
+#ifndef K8_ACQ
+#define K8_ACQ 0
+#endif
 #ifndef K8_SIGNALLER
 #define K8_SIGNALLER 1
 #endif
@@ -525,6 +533,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // K8 with a signaller warp: tiles flushed by each consumer warp (release,
   // CTA scope); the signaller turns them into the GPU-wide done[] counters
   __shared__ unsigned k8_prog[kGroups * kGroupWarps];
+  // the K3 / K8 table pointers, copied once: read through A.k8 every access
+  // was a dependent global load (an L2 round trip after each CCTL.IVALL)
+  __shared__ K8Args k8s;
   const size_t slot_bytes = (size_t)A.block_cap + 8 * (size_t)A.window_cap;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
@@ -536,12 +547,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     loader_k = 0;
+    k8s = *A.k8;
     for (int q = 0; q < kGroups * 4; ++q) k8_arrive[q / 4][q % 4] = 0;
     for (int q = 0; q < kGroups * kGroupWarps; ++q) k8_prog[q] = 0;
   }
   __syncthreads();
   __shared__ unsigned long long zero_target;
-  const bool self_zero = ATOMIC && A.k8->zero_ctr != nullptr;
+  const bool self_zero = ATOMIC && k8s.zero_ctr != nullptr;
   if (self_zero && wid != kGroups * kGroupWarps) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel of the stream is done
     k4_zero_y(A.k8, y, G, wid < kGroups * kGroupWarps ? tid : tid - 32, &zero_target);
@@ -557,7 +569,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       auto ld = [&](int kk, int4& d, int& T) {
         const int tt = blockIdx.x + kk * G;
         if (tt < A.ntiles) {
-          const TileDesc& D = A.tiles[ORDERED ? __ldg(A.k8->order + tt) : tt];
+          const TileDesc& D = A.tiles[ORDERED ? __ldg(k8s.order + tt) : tt];
           const int64_t o = D.block_off;
           d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
           T = D.nrows;
@@ -642,7 +654,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           for (int j = sig; j < m; ++j) {
             const int t = blockIdx.x + (lane + j * kGroups) * G;
-            red_add_u32(A.k8->done + __ldg(A.k8->order + t), (unsigned)kGroupWarps);
+            red_add_u32(k8s.done + __ldg(k8s.order + t), (unsigned)kGroupWarps);
           }
           sig = max(sig, m);
         }
@@ -654,7 +666,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     int k = gw;
     for (int t = blockIdx.x + gw * G; t < A.ntiles; t += NGW * G, k += NGW) {
       const int s = k % NS;
-      const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(A.k8->order + t) : t);
+      const TileDesc* Dg = A.tiles + (ORDERED ? __ldg(k8s.order + t) : t);
       const int row0 = __ldg(&Dg->row0), T = __ldg(&Dg->nrows);
       const int nr = __ldg(&Dg->nruns), ro = __ldg(&Dg->run_off);
       const int gruns = __ldg(&Dg->gather_runs) && !(K4_DBG & 8);
@@ -762,8 +774,31 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
   // flush of every warp waits until all CTAs have zeroed theirs (zero_ctr)
   bool zero_pending = self_zero;
   int k = g;
+  // K8: (tile id, predecessor range) of this warp's current and next tile and
+  // the current tile's predecessor counter index per lane, software-pipelined
+  // so that the acquire loads of the done counters, issued before the stage
+  // waits, are the only global round trip at the top of a tile
+  int4 m_cur = make_int4(0, 0, 0, 0), m_nx = m_cur;
+  int pr_cur = 0;
+  if constexpr (ORDERED) {
+    const int t0 = blockIdx.x + g * G;
+    if (t0 < A.ntiles) {
+      m_cur = __ldg(reinterpret_cast<const int4*>(k8s.pos_meta) + t0);
+      if (m_cur.y + lane < m_cur.z) pr_cur = __ldg(k8s.dag_pred + m_cur.y + lane);
+    }
+  }
   for (int t = blockIdx.x + g * G; t < A.ntiles; t += kGroups * G, k += kGroups) {
     const int s = k % NS;
+    unsigned pv = (unsigned)kGroupWarps;
+    if constexpr (ORDERED) {
+      if (t + kGroups * G < A.ntiles) m_nx = __ldg(reinterpret_cast<const int4*>(k8s.pos_meta) + t + kGroups * G);
+      if (m_cur.y + lane < m_cur.z && !(K4_DBG & 16)) {
+        // acquire: a satisfied counter stays satisfied, so an early look is
+        // valid; unsatisfied ones are polled again before the flush
+        if (K8_ACQ == 0) pv = ld_acquire_u32(k8s.done + pr_cur);
+        else pv = ld_relaxed_u32(k8s.done + pr_cur);
+      }
+    }
     // The parity waits below are safe only once the previous use of stage s
     // (tile k - NS) is complete: a group may finish its previous tile before
     // an older tile's block has landed.  So wait first until tile k - NS has
@@ -795,11 +830,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const uint16_t* sid = reinterpret_cast<const uint16_t*>(blk + D.o_sid);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
-    const int32_t* slot = (ATOMIC || ORDERED) ? nullptr : A.k8->slots + D.spill_off;
+    const int32_t* slot = (ATOMIC || ORDERED) ? nullptr : k8s.slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // flush of window slot l: K4 one RED per (tile, target); K3 own rows
     // stored, spill contributions staged
-    const int tile_id = ORDERED ? __ldg(A.k8->order + t) : t;
+    const int tile_id = ORDERED ? m_cur.x : t;
     if constexpr (ORDERED) {
       // K8, software-pipelined so that no L2 round trip sits between two
       // tiles of a group:
@@ -814,21 +849,37 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       //      per target, so the sum order is fixed and the result bitwise
       //      reproducible; no old-value loads, nothing to wait for;
       //   7. signal the tile (last arriving warp of the group).
-      const int pb = __ldg(A.k8->dag_ptr + tile_id), pe = __ldg(A.k8->dag_ptr + tile_id + 1);
-      unsigned pv = (unsigned)kGroupWarps;
-      if (pb + lane < pe && !(K4_DBG & 16)) pv = ld_acquire_u32(A.k8->done + __ldg(A.k8->dag_pred + pb + lane));
+      // K8_ACQ 0: acquire loads of the predecessors' counters (above, before the
+      // stage waits); 1: relaxed loads there, and the acquire is a
+      // fence.acq_rel.gpu just before the flush (a strong read followed by a
+      // fence is an acquire pattern; measured slower: st27 0.175 vs 0.143 ms)
+      const int pb = m_cur.y, pe = m_cur.z;
       double acc8[kK8Slots];
       int gr8[kK8Slots];
-      bool st8[kK8Slots];
+      unsigned f8[kK8Slots];  // first-writer flags: loaded now, inspected at the flush
+#pragma unroll
+      for (int u = 0; u < kK8Slots; ++u) {
+        const int i = gt + u * kGroupThreads;
+        gr8[u] = -1;
+        f8[u] = 0;
+        if (i < W) {
+          const int l = D.sorted ? (int)sid[i] : i;
+          if (l < T) {
+            gr8[u] = row0 + l;
+            asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(f8[u]) : "l"(k8s.own_first + row0 + l));
+          } else {
+            gr8[u] = tgt[l - T];
+            if (gr8[u] >= 0)
+              asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(f8[u]) : "l"(k8s.slot_first + D.spill_off + (l - T)));
+          }
+        }
+      }
 #pragma unroll
       for (int u = 0; u < kK8Slots; ++u) {
         const int i = gt + u * kGroupThreads;
         acc8[u] = 0.0;
-        gr8[u] = -1;
-        st8[u] = false;
         if (i < W) {
           double acc = 0.0;
-          int l;
           if (!D.sorted) {
             if (i < T) {
               const uint32_t sg = rseg[i];
@@ -842,7 +893,6 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
               const uint32_t q = tcsc[j];
               acc += val[q & 0xffffu] * xs[q >> 16];
             }
-            l = i;
           } else {
             const uint32_t* pseg = reinterpret_cast<const uint32_t*>(blk + D.o_lcol);
             const uint32_t* rec = reinterpret_cast<const uint32_t*>(blk + D.o_tidx);
@@ -853,40 +903,41 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
               const uint32_t q = rec[jb + v];
               acc += val[q & 0xffffu] * xs[q >> 16];
             }
-            l = sid[i];
           }
           acc8[u] = acc;
-          if (l < T) {
-            gr8[u] = row0 + l;
-            st8[u] = __ldg(A.k8->own_first + row0 + l) != 0;
-          } else {
-            gr8[u] = tgt[l - T];
-            st8[u] = gr8[u] >= 0 && __ldg(A.k8->slot_first + D.spill_off + (l - T)) != 0;
-          }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_relaxed(&empty[s]);  // 3. the stage is free
+      // 4. the next tile's predecessor counter index (its meta has arrived)
+      int pr_nx = 0;
+      if (m_nx.y + lane < m_nx.z) pr_nx = __ldg(k8s.dag_pred + m_nx.y + lane);
       if (!(K4_DBG & 16)) {  // 5. (bit 4: diagnostics, no DAG wait)
-        if (!__all_sync(0xffffffffu, pv >= (unsigned)kGroupWarps)) {
+        unsigned okp;  // pv inspected only here: the memory clobber keeps the compare after the sums
+        asm volatile("{\n .reg .pred p;\n setp.ge.u32 p, %1, %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(okp) : "r"(pv), "n"(kGroupWarps) : "memory");
+        if (!__all_sync(0xffffffffu, okp != 0)) {
           for (int q = pb + lane; q < pe; q += 32) {
-            const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
+            const unsigned* f = k8s.done + __ldg(k8s.dag_pred + q);
             while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(32);
           }
           __syncwarp();
         } else {
           for (int q = pb + 32 + lane; q < pe; q += 32) {  // (tiles with > 32 predecessors)
-            const unsigned* f = A.k8->done + __ldg(A.k8->dag_pred + q);
+            const unsigned* f = k8s.done + __ldg(k8s.dag_pred + q);
             while (ld_acquire_u32(f) < (unsigned)kGroupWarps) __nanosleep(32);
           }
           __syncwarp();
         }
+        if (K8_ACQ == 1 && pe > pb) asm volatile("fence.acq_rel.gpu;" ::: "memory");
       }
       if (!(K4_DBG & 4)) {  // 6.
 #pragma unroll
         for (int u = 0; u < kK8Slots; ++u)
           if (gr8[u] >= 0) {
-            if (st8[u] || (K4_DBG & 32)) __stcg(y + gr8[u], acc8[u]);
+            unsigned fv;  // (the memory clobber keeps the flag's first use here, after the sums)
+            asm volatile("mov.b32 %0, %1;" : "=r"(fv) : "r"(f8[u]) : "memory");
+            if (fv != 0 || (K4_DBG & 32)) __stcg(y + gr8[u], acc8[u]);
             else red_add_f64(y + gr8[u], acc8[u]);
           }
       }
@@ -907,9 +958,11 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
                      : "=r"(old) : "r"(smem_u32(&k8_arrive[g][(k / kGroups) & 3])) : "memory");
         if ((old + 1) % (unsigned)kGroupWarps == 0) {
           if (!(K4_DBG & 64)) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // (bit 6: diagnostics, no fence)
-          red_add_u32(A.k8->done + tile_id, (unsigned)kGroupWarps);
+          red_add_u32(k8s.done + tile_id, (unsigned)kGroupWarps);
         }
       }
+      m_cur = m_nx;
+      pr_cur = pr_nx;
     } else {
     auto flush = [&](int l, int sl, double acc) {
       if (K4_DBG & 4) {
@@ -923,7 +976,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       } else if (l < T) {
         y[row0 + l] = acc;
       } else if (sl >= 0) {
-        __stcg(A.k8->spill_buf + sl, acc);
+        __stcg(k8s.spill_buf + sl, acc);
       }
     };
     // one thread per window slot (fixed summation order per slot ->
