@@ -510,8 +510,12 @@ __device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long
 #else
 #define K4_DBG 0
 #endif
-// K8: a dedicated signaller warp (the last gather warp) fences and signals
-// the DAG counters; 0 = the last-arriving consumer warp of a group does it
+// K8 signalling of the DAG counters: 1 = a dedicated signaller warp (the last
+// gather warp); 2 = lanes 1..kGroups of the loader warp (idle otherwise), so
+// all kGatherWarps gather warps keep gathering -- measured slower (st27 0.158
+// vs 0.146 ms, fem 0.286 vs 0.271, spin 0.452 vs 0.409: the divergent lanes
+// delay the loader lane's bulk-copy issue); 0 = the last-arriving consumer
+// warp of a group
 #ifndef K8_ACQ
 #define K8_ACQ 0
 #endif
@@ -552,6 +556,42 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     for (int q = 0; q < kGroups * kGroupWarps; ++q) k8_prog[q] = 0;
   }
   __syncthreads();
+  // ------------------------------------------------ K8 signaller
+  // Lane q < kGroups of the signalling lanes `mask` follows consumer group q.
+  // A group tile j is flushed once all 7 warps of the group have published
+  // progress > j (st.release.cta after their REDs / stores).  Whenever tiles
+  // became complete, ONE fence.acq_rel.gpu (cumulative: it orders the REDs the
+  // acquire loads observed) precedes their done[] signals.  The consumer warps
+  // never wait for their REDs to reach L2 (that wait, one fence per tile on the
+  // consumers' path, was 26% of K8's time on st27).
+  auto k8_signal = [&](const int q, const unsigned mask) {
+    const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
+    const int nq = (q >= 0 && q < kGroups && nk > q) ? (nk - q + kGroups - 1) / kGroups : 0;
+    int sig = 0;  // group tiles of group q already signalled
+    while (__any_sync(mask, sig < nq)) {
+      int m = nq;
+      if (sig < nq) {
+#pragma unroll
+        for (int w = 0; w < kGroupWarps; ++w) {
+          unsigned v;
+          asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+                       : "=r"(v) : "r"(smem_u32(&k8_prog[q * kGroupWarps + w])) : "memory");
+          m = min(m, (int)v);
+        }
+      }
+      const bool any = __any_sync(mask, m > sig);
+      if (!any) {
+        __nanosleep(64);
+        continue;
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (int j = sig; j < m; ++j) {
+        const int t = blockIdx.x + (q + j * kGroups) * G;
+        red_add_u32(k8s.done + __ldg(k8s.order + t), (unsigned)kGroupWarps);
+      }
+      sig = max(sig, m);
+    }
+  };
   __shared__ unsigned long long zero_target;
   const bool self_zero = ATOMIC && k8s.zero_ctr != nullptr;
   if (self_zero && wid != kGroups * kGroupWarps) {
@@ -562,6 +602,14 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // ------------------------------------------------ loader warp (TMA bulk)
     // lane 0 only; (offset, bytes) of the next 4 tiles of this CTA live in a
     // register ring (loop unrolled by 4) so each issue finds its operands ready.
+    if constexpr (ORDERED && K8_SIGNALLER == 2) {
+      // lanes 1..kGroups: the K8 signaller (independent thread scheduling
+      // interleaves them with lane 0's issue loop; both wait by suspending)
+      if (lane >= 1 && lane <= kGroups) {
+        k8_signal(lane - 1, ((1u << kGroups) - 1u) << 1);
+        return;
+      }
+    }
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int4 d0 = make_int4(0, 0, 0, 0), d1 = d0, d2 = d0, d3 = d0;  // (off lo, off hi, bytes, row0)
@@ -623,45 +671,12 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     // copies the unaligned own-x edge elements (the loader bulk-copies the rest).
     const int gw = wid - (kGroups * kGroupWarps + 1);
     if constexpr (ORDERED) {
-      if (K8_SIGNALLER && gw == kGatherWarps - 1) {
-        // ---------------------------------------------- K8 signaller warp
-        // Lane q < kGroups follows consumer group q.  A group tile j is
-        // flushed once all 7 warps of the group have published progress > j
-        // (st.release.cta after their REDs / stores).  Whenever tiles became
-        // complete, ONE fence.acq_rel.gpu (cumulative: it orders the REDs the
-        // acquire loads observed) precedes their done[] signals.  The consumer
-        // warps never wait for their REDs to reach L2 (that wait, one fence
-        // per tile on the consumers' path, was 26% of K8's time on st27).
-        const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
-        const int nq = (lane < kGroups && nk > lane) ? (nk - lane + kGroups - 1) / kGroups : 0;
-        int sig = 0;  // group tiles of lane q's group already signalled
-        while (__any_sync(0xffffffffu, sig < nq)) {
-          int m = nq;
-          if (sig < nq) {
-#pragma unroll
-            for (int w = 0; w < kGroupWarps; ++w) {
-              unsigned v;
-              asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
-                           : "=r"(v) : "r"(smem_u32(&k8_prog[lane * kGroupWarps + w])) : "memory");
-              m = min(m, (int)v);
-            }
-          }
-          const bool any = __any_sync(0xffffffffu, m > sig);
-          if (!any) {
-            __nanosleep(64);
-            continue;
-          }
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          for (int j = sig; j < m; ++j) {
-            const int t = blockIdx.x + (lane + j * kGroups) * G;
-            red_add_u32(k8s.done + __ldg(k8s.order + t), (unsigned)kGroupWarps);
-          }
-          sig = max(sig, m);
-        }
+      if (K8_SIGNALLER == 1 && gw == kGatherWarps - 1) {
+        k8_signal(lane, 0xffffffffu);
         return;
       }
     }
-    constexpr int NGW = (ORDERED && K8_SIGNALLER) ? kGatherWarps - 1 : kGatherWarps;
+    constexpr int NGW = (ORDERED && K8_SIGNALLER == 1) ? kGatherWarps - 1 : kGatherWarps;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // x is ready (PDL prerequisite done)
     int k = gw;
     for (int t = blockIdx.x + gw * G; t < A.ntiles; t += NGW * G, k += NGW) {
