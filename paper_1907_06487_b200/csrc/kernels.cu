@@ -376,10 +376,23 @@ __global__ void __launch_bounds__(256) k_tree(CsrArgs A, ColoredArgs C, TreeArgs
 //       K4 (atomic):        own rows and spill -> RED.F64 into pre-zeroed y.
 // No consumer ever waits on global memory or on another CTA.
 constexpr int kMaxStages = 8;
-constexpr int kGroupWarps = 7;
+// consumer groups x warps per group + gather warps (<= 31 warps + the loader).
+// Measured against the default 4 x 7 + 3 (fem / spin / st27 ms): 4 x 6 + 6:
+// 0.198 / 0.194 / 0.0946 (within noise of 0.199 / 0.197 / 0.0935); 3 x 9 + 3:
+// 0.203 / 0.203 / 0.0966; 2 x 14 + 3: 0.221 / 0.224 / 0.105
+#ifndef K4_GROUP_WARPS
+#define K4_GROUP_WARPS 7
+#endif
+#ifndef K4_GROUPS
+#define K4_GROUPS 4
+#endif
+#ifndef K4_GATHER_WARPS
+#define K4_GATHER_WARPS 3
+#endif
+constexpr int kGroupWarps = K4_GROUP_WARPS;
 constexpr int kGroupThreads = kGroupWarps * 32;
-constexpr int kGroups = 4;
-constexpr int kGatherWarps = 3;
+constexpr int kGroups = K4_GROUPS;
+constexpr int kGatherWarps = K4_GATHER_WARPS;
 constexpr int kTiledThreads = kGroups * kGroupThreads + 32 * (1 + kGatherWarps);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -432,6 +445,15 @@ __device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, unsi
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
+}
+// L2 prefetches (no destination, no completion): issued one to several tiles
+// ahead so that the copy into the ring, which can start only when a stage is
+// free, finds its data in L2 instead of paying a DRAM round trip
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -521,6 +543,23 @@ __device__ __forceinline__ void k4_zero_wait(const K8Args* z, unsigned long long
 #endif
 #ifndef K8_SIGNALLER
 #define K8_SIGNALLER 1
+#endif
+// 1: the gather warps read a short-run tile's spill targets from the block's
+// global copy before the stage wait (0: from the staged block, after it
+// lands); fem_knn_4M K4 0.206 -> 0.199 ms (profiles/r2/i/ab_tgt_global.txt)
+#ifndef K4_TGT_GLOBAL
+#define K4_TGT_GLOBAL 1
+#endif
+// (K3 / K4 only: K8, with two gather warps, measured slower with it on
+// fem_knn_4M, 0.288 vs 0.267 ms)
+#define K4_TGT_G (K4_TGT_GLOBAL && !ORDERED)
+// L2 prefetch (measured slower, off): bit 0 = the loader prefetches the block
+// of the tile 3-4 issues ahead (fem 0.201 vs 0.199 ms, spin 0.207 vs 0.197,
+// st27 0.0975 vs 0.0935); bit 1 = the gather warps prefetch their next tile's
+// own x rows and spill runs / targets before the stage wait (fem 0.210, spin
+// 0.263, st27 0.105) -- profiles/r2/i/ab_prefetch_shapes.txt
+#ifndef K4_PF
+#define K4_PF 0
 #endif
 template <int MODE, int NS>
 __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const double* __restrict__ x,
@@ -621,7 +660,13 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
           const int64_t o = D.block_off;
           d = make_int4((int)(o & 0xffffffff), (int)(o >> 32), D.block_bytes, D.row0);
           T = D.nrows;
+        } else {
+          d.z = 0;
         }
+      };
+      auto pf = [&](const int4& d) {
+        if ((K4_PF & 1) && d.z > 0)
+          bulk_prefetch_l2(A.blocks + ((int64_t)(uint32_t)d.x | ((int64_t)d.y << 32)), (unsigned)d.z);
       };
       auto issue = [&](int k, int4 d, int T) {
         const int s = k % NS, use = k / NS;
@@ -646,16 +691,22 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       ld(3, d3, T3);
       const int nk = (A.ntiles - (int)blockIdx.x + G - 1) / G;  // tiles of this CTA
       for (int kb = 0; kb < nk; kb += 4) {
+        // a descriptor loaded in one step is used for the L2 prefetch in the
+        // next one, so the loader lane never waits for it
         issue(kb, d0, T0);
+        if (kb > 0) pf(d3);
         ld(kb + 4, d0, T0);
         if (kb + 1 >= nk) break;
         issue(kb + 1, d1, T1);
+        pf(d0);
         ld(kb + 5, d1, T1);
         if (kb + 2 >= nk) break;
         issue(kb + 2, d2, T2);
+        pf(d1);
         ld(kb + 6, d2, T2);
         if (kb + 3 >= nk) break;
         issue(kb + 3, d3, T3);
+        pf(d2);
         ld(kb + 7, d3, T3);
       }
     }
@@ -689,10 +740,55 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       // the first batch of run records (8 per lane) is loaded before the stage
       // wait, so its latency overlaps it
       int4 R[8];
+      // short-run tiles (kNN): the first 1024 spill targets are read from the
+      // block's global copy into the same registers, also before the stage
+      // wait, so the x gather no longer waits for the tile block to land (the
+      // chain stage free -> block -> targets -> x was two DRAM round trips)
+      const int Sg = (gruns || !K4_TGT_G) ? 0 : __ldg(&Dg->nspill);
+      const int32_t* tgt_g =
+          K4_TGT_G ? reinterpret_cast<const int32_t*>(A.blocks + __ldg(&Dg->block_off) + __ldg(&Dg->o_tgt)) : nullptr;
+      if (K4_TGT_G && !gruns) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int r = u * 32 + lane;
-        R[u] = (gruns && r < nr) ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
+        for (int u = 0; u < 8; ++u) {
+          const int i0 = u * 128 + lane;
+          R[u].x = i0 < Sg ? __ldg(tgt_g + i0) : -1;
+          R[u].y = i0 + 32 < Sg ? __ldg(tgt_g + i0 + 32) : -1;
+          R[u].z = i0 + 64 < Sg ? __ldg(tgt_g + i0 + 64) : -1;
+          R[u].w = i0 + 96 < Sg ? __ldg(tgt_g + i0 + 96) : -1;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = u * 32 + lane;
+          R[u] = (gruns && r < nr) ? __ldg(reinterpret_cast<const int4*>(A.runs) + ro + r) : make_int4(0, 0, 0, 0);
+        }
+      }
+      if (K4_PF & 2) {
+        // x of this tile into L2 while the stage is still in use
+        if (lane == 2 && T > 0) {
+          const double* xa = x + row0 + (int)(((uintptr_t)(x + row0) >> 3) & 1);
+          const int nf = (T - (int)(xa - (x + row0))) & ~1;
+          if (nf > 0) bulk_prefetch_l2(xa, (unsigned)nf * 8u);
+        }
+        if (gruns) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int len = R[u].z;
+            if (len <= 0) continue;
+            const double* src = x + R[u].x;
+            const int i0 = (int)(((uintptr_t)src >> 3) & 1);
+            const int nb = len > i0 ? ((len - i0) & ~1) : 0;
+            if (nb > 0) bulk_prefetch_l2(src + i0, (unsigned)nb * 8u);
+          }
+        } else if (K4_TGT_G) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (R[u].x >= 0) prefetch_l2(x + R[u].x);
+            if (R[u].y >= 0) prefetch_l2(x + R[u].y);
+            if (R[u].z >= 0) prefetch_l2(x + R[u].z);
+            if (R[u].w >= 0) prefetch_l2(x + R[u].w);
+          }
+        }
       }
       // stage free: tile k - NS has been consumed.  With NS % kGatherWarps ==
       // 0 an mbarrier wait (hardware suspend) replaces the poll of loader_k,
@@ -759,6 +855,20 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
             if (i0) cp_async8(dst, src);
             if (i0 + nb < len) cp_async8(dst + len - 1, src + len - 1);
           }
+        }
+      } else if (K4_TGT_G) {
+        // short runs: slot by slot, targets already in registers
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i0 = u * 128 + lane;
+          if (R[u].x >= 0) cp_async8(xs + T + i0, x + R[u].x);
+          if (R[u].y >= 0) cp_async8(xs + T + i0 + 32, x + R[u].y);
+          if (R[u].z >= 0) cp_async8(xs + T + i0 + 64, x + R[u].z);
+          if (R[u].w >= 0) cp_async8(xs + T + i0 + 96, x + R[u].w);
+        }
+        for (int idx = 1024 + lane; idx < Sg; idx += 32) {
+          const int g = __ldg(tgt_g + idx);
+          if (g >= 0) cp_async8(xs + T + idx, x + g);
         }
       } else {
         // short runs: slot by slot from the block's target list, spread over the lanes
