@@ -598,7 +598,24 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     const int32_t vb = (int32_t)(D.o_val / 8);  // bank-pair phase of val[0]
     // sorted tiles walk one list per lane (row part, then transposed part) in
     // lock step; unsorted tiles walk the two parts as separate lock-step loops
-    auto rlen = [&](int32_t l) { return (uni && l < T) ? rl[(size_t)l] : 0; };
+    // Sorted tiles carry explicit (val index | x index) records, so a lane's
+    // row records need not come first: they join the lane's list and the
+    // bank-aware pick below orders all of a lane's records (SYMM_REC_FREE=0:
+    // row records first, in row order).
+    const bool rec_free = uni && (!std::getenv("SYMM_REC_FREE") || std::atoi(std::getenv("SYMM_REC_FREE")) != 0);
+    if (rec_free)
+      for (int32_t l = 0; l < T; ++l) {
+        std::vector<uint32_t> all;
+        for (int32_t k = rst[(size_t)l]; k < rst[(size_t)l] + rl[(size_t)l]; ++k) all.push_back((uint32_t)k | ((uint32_t)lcol[k] << 16));
+        all.insert(all.end(), lists[(size_t)l].begin(), lists[(size_t)l].end());
+        lists[(size_t)l].swap(all);
+      }
+    auto rlen = [&](int32_t l) { return (uni && !rec_free && l < T) ? rl[(size_t)l] : 0; };
+    // SYMM_VAL_COLOR=1 (sorted tiles): the record order is chosen for the x
+    // gathers alone, and the val array is then permuted so that the entries a
+    // half warp reads in one lock step sit in distinct bank pairs (below)
+    const bool val_color = rec_free && bank_aware && std::getenv("SYMM_VAL_COLOR") && std::atoi(std::getenv("SYMM_VAL_COLOR")) != 0;
+    const int vw = val_color ? 0 : 1;  // weight of the val banks in the pick
     if (bank_aware)
       for (int32_t g0 = 0; g0 < W; g0 += 32) {
         const int32_t g1 = std::min(W, g0 + 32);
@@ -672,15 +689,15 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
                 size_t bq = jj;
                 int bsc = INT32_MAX;
                 for (size_t e = jj; e < L.size(); ++e) {
-                  const int sc = 4 * (cv[((L[e] & 0xffffu) + vb) & 15] + cr[(L[e] >> 16) & 15]) +
-                                 (cv[((L[e] & 0xffffu) + vb) & 15] > 0) + (cr[(L[e] >> 16) & 15] > 0);
+                  const int sc = 4 * (vw * cv[((L[e] & 0xffffu) + vb) & 15] + cr[(L[e] >> 16) & 15]) +
+                                 vw * (cv[((L[e] & 0xffffu) + vb) & 15] > 0) + (cr[(L[e] >> 16) & 15] > 0);
                   if (sc < bsc) { bsc = sc; bq = e; if (sc == 0) break; }
                 }
                 pick[ord[q]] = bq;
                 cv[((L[bq] & 0xffffu) + vb) & 15]++;
                 cr[(L[bq] >> 16) & 15]++;
               }
-              const int cost = *std::max_element(cv, cv + 16) + *std::max_element(cr, cr + 16);
+              const int cost = vw * *std::max_element(cv, cv + 16) + *std::max_element(cr, cr + 16);
               if (cost < best_cost) {
                 best_cost = cost;
                 std::copy(pick, pick + na, best_pick);
@@ -692,6 +709,57 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
             }
           }
       }
+    if (val_color) {
+      // Every stored entry is read by two records (its row's lane and its
+      // column's lane; the diagonal by one), i.e. in at most two (half warp,
+      // lock step) groups.  Entries are given one of the 16 bank pairs
+      // greedily -- the pair least used in their two groups, among the pairs
+      // that still have free positions -- and val is permuted accordingly.
+      const bool rem_last = !peel_sorted && place_peel;
+      int32_t TM = 2;
+      for (int32_t i = 0; i < W; ++i) TM = std::max<int32_t>(TM, (int32_t)lists[(size_t)slot_at[(size_t)i]].size() + 2);
+      const int32_t nhalf = (W + 15) / 16;
+      std::vector<uint8_t> cnt((size_t)nhalf * (size_t)TM * 16, 0);
+      std::vector<int32_t> grp((size_t)nnz * 2, -1);
+      for (int32_t g0 = 0; g0 < W; g0 += 32) {
+        const int32_t g1 = std::min(W, g0 + 32);
+        int32_t B = 0;
+        for (int32_t i = g0; i < g1; ++i)
+          B = std::max<int32_t>(B, (int32_t)lists[(size_t)slot_at[(size_t)i]].size() & ~(kK4SortedUnroll - 1));
+        for (int32_t i = g0; i < g1; ++i) {
+          const auto& L = lists[(size_t)slot_at[(size_t)i]];
+          const int32_t n = (int32_t)L.size(), nb = n & ~(kK4SortedUnroll - 1);
+          for (int32_t v = 0; v < n; ++v) {
+            const int32_t tau = (rem_last && v >= nb) ? B + (v - nb) : v;
+            const int32_t e = (int32_t)(L[(size_t)v] & 0xffffu);
+            grp[(size_t)e * 2 + (grp[(size_t)e * 2] >= 0 ? 1 : 0)] = (i / 16) * TM + tau;
+          }
+        }
+      }
+      int32_t cap[16] = {0}, used[16] = {0};
+      for (int32_t p2 = 0; p2 < nnz; ++p2) cap[(p2 + vb) & 15]++;
+      std::vector<int32_t> newpos((size_t)nnz, -1);
+      for (int32_t e = 0; e < nnz; ++e) {
+        const int32_t a = grp[(size_t)e * 2], b2 = grp[(size_t)e * 2 + 1];
+        if (a < 0) continue;  // pad entry: read by nobody
+        int best = -1, bsc = INT32_MAX;
+        for (int c = 0; c < 16; ++c) {
+          if (used[c] >= cap[c]) continue;
+          const int sc = 64 * ((int)cnt[(size_t)a * 16 + c] + (b2 >= 0 ? (int)cnt[(size_t)b2 * 16 + c] : 0)) - std::min(63, cap[c] - used[c]);
+          if (sc < bsc) { bsc = sc; best = c; }
+        }
+        cnt[(size_t)a * 16 + best]++;
+        if (b2 >= 0) cnt[(size_t)b2 * 16 + best]++;
+        newpos[(size_t)e] = ((best - vb) & 15) + 16 * used[best]++;
+      }
+      std::vector<double> nv((size_t)nnz, 0.0);
+      for (int32_t e = 0; e < nnz; ++e)
+        if (newpos[(size_t)e] >= 0) nv[(size_t)newpos[(size_t)e]] = val[e];
+      std::copy(nv.begin(), nv.end(), val);
+      for (int32_t l = 0; l < W; ++l)
+        for (uint32_t& q : lists[(size_t)l]) q = (q & 0xffff0000u) | (uint32_t)newpos[(size_t)(q & 0xffffu)];
+      for (int32_t l = 0; l < T; ++l) rseg[l] = 0;  // (sorted tiles never read rseg; val is no longer in row order)
+    }
     if (!D.sorted) {
       int32_t pos = 0;
       for (int32_t i = 0; i < W; ++i) {
@@ -707,7 +775,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
       for (int32_t i = 0; i < W; ++i) {
         const int32_t l = slot_at[(size_t)i];
         int32_t q = pst[i];
-        const int32_t nrow = l < T ? rl[(size_t)l] : 0;
+        const int32_t nrow = (l < T && !rec_free) ? rl[(size_t)l] : 0;
         for (int32_t k = 0; k < nrow; ++k) {
           const int32_t e = rst[(size_t)l] + k;
           tcsc[q++] = (uint32_t)e | ((uint32_t)lcol[e] << 16);

@@ -92,7 +92,7 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
             assert np.array_equal(gid[w:w + ln], g + np.arange(ln))
             if int(D["gather_runs"]):
                 assert (w - (g - row0)) % 2 == 0
-        if nnz > int(rln.sum()):  # padded placement: the unrolled steps of a half warp's rows
+        if not srt and nnz > int(rln.sum()):  # padded placement: the unrolled steps of a half warp's rows
             # (which begin after each lane's loop-length % 4 leftover steps) start on distinct bank pairs
             for g0 in range(0, W, 16):
                 idx = [i for i in range(g0, min(W, g0 + 16)) if sid[i] < T]
@@ -103,37 +103,43 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
                 res = [(int(D["o_val"]) // 8 + int(rst[sid[i]]) + (0 if srt else nl & (K4_UNROLL - 1))) % 16
                        for i, nl in zip(idx, n_loop)]
                 assert len(set(res)) == len(res)
-        if srt:  # the row records give every entry's local column
-            for i in range(W):
-                l = int(sid[i])
-                if l < T:
-                    for u in range(int(rln[l])):
-                        q = int(rec[int(pseg[i] & 0xFFFF) + u])
-                        assert q & 0xFFFF == rst[l] + u
-                        lcol[q & 0xFFFF] = q >> 16
+        if srt:
+            # a lane's record list holds (val index | x window id) records in any order: row
+            # records of own row l (entry (l, c), c >= l in upper storage, x window id of c) and
+            # transposed records (entry (r, l), r < l an own row, x window id of r); the val array
+            # of a sorted tile may be permuted (bank-pair colouring), rseg is not used
+            uses = np.zeros(nnz, dtype=np.int64)
         for i in range(W):
             l = int(sid[i])
             acc = 0.0
-            if l < T:
-                for k in range(int(rst[l]), int(rst[l] + rln[l])):
-                    acc += val[k] * xs[lcol[k]]              # tmp += A[idx] x[col[idx]]
-                    row_pairs.append((row0 + l, int(gid[lcol[k]])))
             if srt:
-                cb = int(pseg[i] & 0xFFFF) + (int(rln[l]) if l < T else 0)
-                ce = int(pseg[i] & 0xFFFF) + int(pseg[i] >> 16)
-                csc_list = rec[cb:ce]
+                lst = rec[int(pseg[i] & 0xFFFF):int(pseg[i] & 0xFFFF) + int(pseg[i] >> 16)]
+                for q in lst:
+                    e, xi = int(q) & 0xFFFF, int(q) >> 16
+                    uses[e] += 1
+                    acc += val[e] * xs[xi]
+                    if l < T and gid[xi] >= row0 + l:   # tmp += A[idx] x[col[idx]]
+                        row_pairs.append((row0 + l, int(gid[xi])))
+                    else:                               # b[col] += A[idx] x[row]
+                        assert xi < T
+                        csc_pairs.append((row0 + xi, int(gid[l])))
             else:
-                csc_list = tcsc[int(tptr[i]):int(tptr[i + 1])]
-            for q in csc_list:
-                q = int(q)
-                e, r = q & 0xFFFF, q >> 16
-                assert r < T and lcol[e] == l and rst[r] <= e < rst[r] + rln[r]
-                acc += val[e] * xs[r]                          # b[col] += A[idx] x[row]
-                csc_pairs.append((row0 + r, int(gid[l])))
+                if l < T:
+                    for k in range(int(rst[l]), int(rst[l] + rln[l])):
+                        acc += val[k] * xs[lcol[k]]              # tmp += A[idx] x[col[idx]]
+                        row_pairs.append((row0 + l, int(gid[lcol[k]])))
+                for q in tcsc[int(tptr[i]):int(tptr[i + 1])]:
+                    q = int(q)
+                    e, r = q & 0xFFFF, q >> 16
+                    assert r < T and lcol[e] == l and rst[r] <= e < rst[r] + rln[r]
+                    acc += val[e] * xs[r]                          # b[col] += A[idx] x[row]
+                    csc_pairs.append((row0 + r, int(gid[l])))
             if gid[l] >= 0:
                 y[gid[l]] += acc
             else:
                 assert acc == 0.0
+        if srt:
+            assert uses.max(initial=0) <= 2  # an entry: once by its row's lane, once by its column's
     return y, row_pairs, csc_pairs
 
 
