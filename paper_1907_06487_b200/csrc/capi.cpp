@@ -599,10 +599,14 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     // sorted tiles walk one list per lane (row part, then transposed part) in
     // lock step; unsorted tiles walk the two parts as separate lock-step loops
     // Sorted tiles carry explicit (val index | x index) records, so a lane's
-    // row records need not come first: they join the lane's list and the
-    // bank-aware pick below orders all of a lane's records (SYMM_REC_FREE=0:
-    // row records first, in row order).
-    const bool rec_free = uni && (!std::getenv("SYMM_REC_FREE") || std::atoi(std::getenv("SYMM_REC_FREE")) != 0);
+    // row records need not come first.  Opt-in (SYMM_REC_FREE=1 or
+    // SYMM_VAL_COLOR=1): they join the lane's list and the bank-aware pick
+    // below orders all of a lane's records.  Measured on fem_knn_4M (B200,
+    // profiles/r2/i/ab_val_color.txt): the model's val / x conflict factors
+    // drop from 1.79 / 1.82 to 1.60 / 1.70 with the colouring, the time stays
+    // at 0.196-0.201 ms either way, so the default keeps row records first.
+    const bool rec_free = uni && ((std::getenv("SYMM_REC_FREE") && std::atoi(std::getenv("SYMM_REC_FREE")) != 0) ||
+                                  (std::getenv("SYMM_VAL_COLOR") && std::atoi(std::getenv("SYMM_VAL_COLOR")) != 0));
     if (rec_free)
       for (int32_t l = 0; l < T; ++l) {
         std::vector<uint32_t> all;

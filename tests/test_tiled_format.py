@@ -175,6 +175,26 @@ def test_tiled_format_decodes_to_oracle(name, gain, monkeypatch):
     assert sorted(csc_pairs) == off_pairs   # every off-diagonal entry once in its column's lane
 
 
+@pytest.mark.parametrize("name", ["fem_knn_30k", "st27_24"])
+def test_tiled_format_val_colouring(name, monkeypatch):
+    """Opt-in format of sorted tiles (SYMM_VAL_COLOR=1): records in free order, val permuted so
+    that a half warp's lock-step val loads hit distinct bank pairs -- same product, every entry
+    still read once by its row's lane and once by its column's lane."""
+    monkeypatch.setenv("SYMM_VAL_COLOR", "1")
+    monkeypatch.setenv("SYMM_SORT_GAIN", "0")
+    U, x = gen.make_config(name)
+    s = P.build_schedule(U)
+    perm, inv = s.permutation()
+    desc, blocks, runs, targets = dump(s)
+    assert desc["sorted"].any()
+    y, row_pairs, csc_pairs = decode_and_multiply(desc, blocks, runs, targets, U.n, x[inv])
+    y_ref = oracle.symmspmv(U, x)
+    assert np.max(np.abs(y[perm] - y_ref)) / np.max(np.abs(y_ref)) <= 1e-13
+    all_pairs, off_pairs = permuted_pairs(s, U)
+    assert sorted(row_pairs) == all_pairs
+    assert sorted(csc_pairs) == off_pairs
+
+
 def test_tiled_format_edge_cases():
     for U in (gen.from_edges(1, [], [], [], [2.5]), gen.path(200), gen.random_symmetric(300, 1.1, 12),
               gen.from_edges(120, [0] * 119, list(range(1, 120)))):

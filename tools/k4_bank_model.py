@@ -10,6 +10,7 @@ import sys
 
 import numpy as np
 
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests"))
 import gen  # noqa: E402
 import paper_1907_06487_b200 as P  # noqa: E402
