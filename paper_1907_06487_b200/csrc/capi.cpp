@@ -243,6 +243,11 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     slot_ptr[(size_t)t + 1] = slot_ptr[(size_t)t] + w;
     run_ptr[(size_t)t + 1] = run_ptr[(size_t)t] + nr;
   }
+  // single-run tiles carry no tgt[] in their block (TileDesc.gather_runs bit 1)
+  const bool single_on = !std::getenv("SYMM_SINGLE_RUN") || std::atoi(std::getenv("SYMM_SINGLE_RUN")) != 0;
+  std::vector<char> single_run((size_t)nt, 0);
+  for (int32_t t = 0; t < nt; ++t)
+    single_run[(size_t)t] = single_on && use_runs[(size_t)t] && run_ptr[(size_t)t + 1] - run_ptr[(size_t)t] == 1;
   std::vector<int32_t> slot_tgt((size_t)slot_ptr[(size_t)nt], -1);
   std::vector<char> slot_first((size_t)slot_ptr[(size_t)nt], 0);  // this tile writes the target first (lowest phase)
 
@@ -422,7 +427,7 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
       L.o_sid = align16(L.o_tidx + 4 * L.nrec);
       L.o_tgt = align16(L.o_sid + 2 * W);
     }
-    L.o_val = align16(L.o_tgt + 4 * S_);
+    L.o_val = align16(L.o_tgt + (single_run[(size_t)t] ? 0 : 4 * S_));
     L.bytes = align16(L.o_val + 8 * L.nnz);
     return L;
   };
@@ -478,6 +483,12 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     D.run_off = (int32_t)run_ptr[(size_t)t];
     D.nruns = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);
     D.gather_runs = use_runs[(size_t)t];
+    if (single_run[(size_t)t]) {
+      const SpillRun& R = runs[(size_t)run_ptr[(size_t)t]];
+      D.gather_runs |= 2 | (R.wid > T ? 4 : 0);  // (at most one parity pad slot before the run)
+      D.tgt_base = R.row - R.wid;
+      if (R.wid - T > 1 || R.wid - T + R.len != S_) { bad = t + 1; break; }
+    }
     boff[(size_t)t + 1] = boff[(size_t)t] + bytes;
     D.block_off = boff[(size_t)t];
     block_cap = std::max<int32_t>(block_cap, (int32_t)bytes);
@@ -518,7 +529,8 @@ int build_tiled_host(const Schedule& S, int32_t t_begin, int32_t t_end, TiledHos
     double* val = reinterpret_cast<double*>(blk + D.o_val);
     const int32_t* st = slot_tgt.data() + slot_ptr[(size_t)t];
     // flush target of every spill slot (-1 = pad)
-    for (int32_t j = 0; j < ns; ++j) tgt[j] = st[j];
+    if (!(D.gather_runs & 2))
+      for (int32_t j = 0; j < ns; ++j) tgt[j] = st[j];
     const int32_t e0 = S.prow_ptr[(size_t)r0];
     const SpillRun* tr = runs.data() + run_ptr[(size_t)t];
     const int32_t nrt = (int32_t)(run_ptr[(size_t)t + 1] - run_ptr[(size_t)t]);

@@ -105,10 +105,14 @@ struct TileDesc {
   int32_t spill_off;    // first spill slot of this tile (targets / slots arrays)
   int32_t run_off;      // first run of this tile (runs array)
   int32_t nruns;        // runs of consecutive spill targets
-  int32_t gather_runs;  // 1: the gather warps bulk-copy the runs (long runs); 0: they
-                        // cp.async slot by slot from the block's tgt list (short runs)
+  int32_t gather_runs;  // bit 0: the gather warps bulk-copy the runs (long runs); else they
+                        // cp.async slot by slot from the block's tgt list (short runs).
+                        // bit 1: single-run tile -- the spill window is ONE run of consecutive
+                        // rows (every tile of a stencil in BFS order), so the block carries no
+                        // tgt[]: window slot l >= T + (bit 2) flushes to row tgt_base + l, the
+                        // slot before it (bit 2: one parity pad) to nothing
   int32_t sorted;       // 1: lanes take the window slots in the order sid[] (work-sorted)
-  int32_t pad;
+  int32_t tgt_base;     // single-run tiles: first row of the run - its window id
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc must be 64 B");
 

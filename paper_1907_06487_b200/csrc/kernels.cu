@@ -955,6 +955,9 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
     const uint16_t* tptr = reinterpret_cast<const uint16_t*>(blk + D.o_tptr);
     const uint16_t* sid = reinterpret_cast<const uint16_t*>(blk + D.o_sid);
     const int32_t* tgt = reinterpret_cast<const int32_t*>(blk + D.o_tgt);
+    // single-run tiles have no tgt[]: slot l >= wpad flushes to row tgt_base + l
+    const int srun = D.gather_runs >> 1, tgt_base = D.tgt_base, wpad = T + (srun >> 1);
+    auto spill_row = [&](int l) { return srun ? (l < wpad ? -1 : tgt_base + l) : tgt[l - T]; };
     const int32_t* slot = (ATOMIC || ORDERED) ? nullptr : k8s.slots + D.spill_off;
     const double* val = reinterpret_cast<const double*>(blk + D.o_val);
     // flush of window slot l: K4 one RED per (tile, target); K3 own rows
@@ -993,7 +996,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
             gr8[u] = row0 + l;
             asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(f8[u]) : "l"(k8s.own_first + row0 + l));
           } else {
-            gr8[u] = tgt[l - T];
+            gr8[u] = spill_row(l);
             if (gr8[u] >= 0)
               asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(f8[u]) : "l"(k8s.slot_first + D.spill_off + (l - T)));
           }
@@ -1093,7 +1096,7 @@ __global__ void __launch_bounds__(kTiledThreads, 1) k_tiled(TiledArgs A, const d
       if (K4_DBG & 4) {
         // diagnostics: no flush
       } else if (ATOMIC) {
-        const int gr = l < T ? row0 + l : tgt[l - T];
+        const int gr = l < T ? row0 + l : spill_row(l);
 #ifdef K4_CHECK
         if (gr >= A.check_n) { printf("K4_CHECK flush t=%d l=%d gr=%d\n", t, l, gr); __trap(); }
 #endif

@@ -25,7 +25,7 @@ from paper_1907_06487_b200._lib import check, lib  # noqa: E402
 DESC = np.dtype([("block_off", "<i8"), ("block_bytes", "<i4"), ("nrows", "<i4"), ("nspill", "<i4"), ("nnz", "<i4"),
                  ("row0", "<i4"), ("o_lcol", "<u2"), ("o_tidx", "<u2"), ("o_tptr", "<u2"), ("o_tgt", "<u2"),
                  ("o_sid", "<u2"), ("o_val", "<u2"), ("spill_off", "<i4"), ("run_off", "<i4"), ("nruns", "<i4"),
-                 ("gather_runs", "<i4"), ("sorted", "<i4"), ("pad", "<i4")])
+                 ("gather_runs", "<i4"), ("sorted", "<i4"), ("tgt_base", "<i4")])
 assert DESC.itemsize == 64
 RUN = np.dtype([("row", "<i4"), ("wid", "<i4"), ("len", "<i4"), ("pad", "<i4")])
 
@@ -73,7 +73,14 @@ def decode_and_multiply(desc, blocks, runs, targets, n, xp):
             nrec = int(((pseg & 0xFFFF) + (pseg >> 16)).max(initial=0))
             rec = np.frombuffer(b, dtype="<u4", count=nrec, offset=h + int(D["o_tidx"])).astype(np.int64)
             lcol = np.full(nnz, -1, dtype=np.int64)
-        tgt = np.frombuffer(b, dtype="<i4", count=S, offset=h + int(D["o_tgt"])).astype(np.int64)
+        if int(D["gather_runs"]) & 2:
+            # single-run tile: no tgt[] in the block; window slot l >= T + npad flushes to row
+            # tgt_base + l, the parity pad slot before it (if any) to nothing
+            npad = (int(D["gather_runs"]) >> 2) & 1
+            assert int(D["nruns"]) == 1 and int(D["o_tgt"]) + 15 >= int(D["o_val"]) - 16
+            tgt = np.concatenate([np.full(npad, -1, dtype=np.int64), int(D["tgt_base"]) + T + np.arange(npad, S)])
+        else:
+            tgt = np.frombuffer(b, dtype="<i4", count=S, offset=h + int(D["o_tgt"])).astype(np.int64)
         assert np.array_equal(tgt, targets[int(D["spill_off"]):int(D["spill_off"]) + S])
         val = np.frombuffer(b, dtype="<f8", count=nnz, offset=h + int(D["o_val"]))
         if int(D["sorted"]):
@@ -152,7 +159,7 @@ def permuted_pairs(s, U):
     return sorted(zip(rows.tolist(), col.tolist())), sorted(zip(rows[col != rows].tolist(), col[col != rows].tolist()))
 
 
-@pytest.mark.parametrize("name", ["lap2d_64", "st27_24", "spin_14", "fem_knn_30k"])
+@pytest.mark.parametrize("name", ["lap2d_64", "lap3d_40", "st27_24", "spin_14", "fem_knn_30k"])
 @pytest.mark.parametrize("gain", ["0.25", "0", "1"])
 def test_tiled_format_decodes_to_oracle(name, gain, monkeypatch):
     monkeypatch.setenv("SYMM_SORT_GAIN", gain)  # sorted lanes: default rule / every tile / never
